@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one fused Vecchia loglik + gradient + Fisher-information
+evaluation per step (BASELINE.json metric: observations / second at n = 2^20, m = 30).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[1]): n = 2^20 uniform points in [0,1]^2 PER GPU (weak
+scaling: n_total = N * 2^20, contiguous row shards, dataset replicated), p = 1, Matern 3/2
+("matern15_isotropic"), theta = (1.0, 0.05, 0.1), m = 30, synthetic y ~ N(0,1), neighbor
+table from the package's own host search.  One JSON line is printed by rank 0.
+
+`value`     : obs/s with inputs resident in HBM; K steps timed with CUDA events, max over ranks.
+`e2e`       : obs/s through the public API (engine.DeviceProblem from pinned HOST arrays ->
+              evaluation -> totals on the host), H2D and D2H inside the timed region.
+`roofline`  : the main kernel against the measured FP64 (DFMA) peak of this GPU.
+`cpu_baseline` / `--impl reference`: the CPU implementation of the same path on the host
+              cores (oracle port for Matern, which the reference lacks; the reference's own
+              compiled core, oracle/_ref, is timed beside it on the exponential kernel).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "Vecchia loglik+grad+info evals: obs/sec at n=2^20, m=30"
+UNIT = "obs/s"
+
+
+def algorithmic_flops(family: str, d: int, p: int, q: int, m: int) -> dict:
+    """flops per tail observation, every + - * / sqrt exp log = 1,
+    FMA = 2, distance/exp once per pair.  F_min counts the variance/nugget shortcuts this
+    kernel uses (c_0 = e_last/sigma^2, c_nugget = sigma^2 B^-1 u)."""
+    k = m + 1
+    T = k * (k - 1) // 2
+    pair = {"exponential_isotropic": 3 * d + 6, "exponential_sphere": 3 * d + 6, "matern15_isotropic": 3 * d + 10,
+            "matern25_isotropic": 3 * d + 13, "exponential_spacetime": 4 * d + 11,
+            "exponential_anisotropic": 4 * d + 8 + 3 * d}[family]
+    qd = q - 2
+    cov = T * pair + 2 * k
+    chol = sum((a + 1) ** 2 for a in range(k))
+    solves = (2 + p) * k * k
+    dense = 4 * T + k + k * k
+    contract = (2 + p + p * p) + q * (2 * k + 2 * k * p + 5 + 5 * p + 5 * p * p) + q * (q + 1) // 2 * (2 * k + 2)
+    return {"F_generic": cov + chol + solves + q * dense + contract,
+            "F_min": cov + chol + solves + qd * dense + (k + k * k) + contract}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_power_cap": 0x4, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "hw_power_brake_slowdown": 0x80, "sync_boost": 0x10, "applications_clocks_setting": 0x2}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(int(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                mask = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                for name, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_workload(n_total: int, d: int, p: int, seed: int = 2407):
+    rng = np.random.default_rng(seed)
+    locs = rng.uniform(0.0, 1.0, (n_total, d))
+    y = rng.normal(size=n_total)
+    X = np.ones((n_total, p))
+    if p > 1:
+        X[:, 1:] = locs[:, :p - 1]
+    return y, X, locs
+
+
+def cpu_time_oracle(y, X, locs, nn_rows, row0, family, theta, rows, workers, repeats=1):
+    """Best-of timing of the C oracle port over `rows` observations starting at row0."""
+    from oracle import vecchia_oracle as vo
+    n = y.shape[0]
+    full = np.full((n, nn_rows.shape[1]), -1, dtype=np.int64)  # oracle indexes the table by global row
+    full[row0:row0 + nn_rows.shape[0]] = nn_rows
+    best = float("inf")
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        vo.run(y, X, locs, full, family, theta, i0=row0, i1=row0 + rows, workers=workers, deterministic=False)
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def reference_arm(args):
+    """--impl reference: the CPU implementation of the same evaluation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import reference_core, vecchia_oracle as vo
+    cores = os.cpu_count() or 1
+    n_total = args.gpus * args.n
+    y, X, locs = make_workload(n_total, args.d, args.p)
+    theta = np.asarray(args.theta, dtype=np.float64)
+    # bounded sample: the first `sample` rows past the ragged head, sized for ~2 s per step
+    from paper_2407_02740_b200.preprocess import find_ordered_neighbor_rows
+    probe = 1 << 14
+    row0 = n_total // 2
+    nn_probe = find_ordered_neighbor_rows(locs, args.m, row0, probe)
+    t = cpu_time_oracle(y, X, locs, nn_probe, row0, args.family, theta, probe, cores)
+    sample = int(min(n_total - row0, max(probe, (probe / t) * args.ref_seconds)))
+    sample = 1 << int(np.floor(np.log2(sample)))
+    nn_rows = find_ordered_neighbor_rows(locs, args.m, row0, sample)
+    for _ in range(args.warmup):
+        cpu_time_oracle(y, X, locs, nn_rows, row0, args.family, theta, sample, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_time_oracle(y, X, locs, nn_rows, row0, args.family, theta, sample, cores)
+    sec = (time.perf_counter() - t0) / args.steps
+    value = sample / sec
+    kind = "port"
+    extra = {}
+    if reference_core.available():
+        # the reference's own compiled core has no Matern kernel: time it on the exponential
+        # kernel over the same rows as context (same gather / Cholesky / solves, cheaper pair term)
+        full = np.full((n_total, args.m + 1), -1, dtype=np.int64)
+        full[row0:row0 + sample] = nn_rows
+        K = reference_core.module()
+        q, pp, L = 3, args.p, 0
+        slots = (np.zeros(n_total), np.zeros(n_total), np.zeros((n_total, pp, pp)), np.zeros((n_total, pp)),
+                 np.zeros((n_total, q)), np.zeros((n_total, q)), np.zeros((n_total, pp, q)),
+                 np.zeros((n_total, pp, pp, q)), np.zeros((n_total, q, q))) if n_total <= (1 << 21) else None
+        if slots is not None:
+            failv = np.zeros(n_total, dtype=np.int32)
+            th = np.array([theta[0], theta[1], theta[-1]])
+            best = float("inf")
+            for _ in range(2):
+                t1 = time.perf_counter()
+                K.RUNNERS["task"](y, X, locs, full, th, 0, 0.0, slots, failv, row0, row0 + sample, cores, 32)
+                best = min(best, time.perf_counter() - t1)
+            extra["reference_compiled_core_exp_iso_obs_per_s"] = sample / best
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * sec, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, n_total),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"rows [{row0}, {row0 + sample}) of the same workload per step "
+                                   f"(C/OpenMP port of the reference kernel with the Matern 3/2 pair term; "
+                                   f"the reference itself has no Matern family)", **extra},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, n_total):
+    return {"workload": f"config2: n={args.n} per GPU ({n_total} total), d={args.d}, p={args.p}, "
+                        f"{args.family}, m={args.m}, theta={list(args.theta)}, one loglik+grad+info evaluation per step",
+            "n_per_gpu": args.n, "n_total": n_total, "m": args.m, "family": args.family, "d": args.d, "p": args.p,
+            "parallelism": f"observation shards x{args.gpus}, one all-reduce of L+1 doubles",
+            "l2_policy": "inputs larger than L2 (neighbor table %.0f MB per GPU streamed once per step)"
+                         % (args.n * (args.m + 1) * 8 / 1e6)}
+
+
+def ours_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_02740_b200 as vg
+    from paper_2407_02740_b200 import _cabi, distributed, engine
+    from paper_2407_02740_b200.preprocess import find_ordered_neighbor_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise vg.DeviceUnavailable("bench.py needs a CUDA device: the cuda core has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    n_total = world * args.n
+    theta = np.asarray(args.theta, dtype=np.float64)
+    q = theta.shape[0]
+    y, X, locs = make_workload(n_total, args.d, args.p)
+    i0, i1 = distributed.shard_bounds(n_total, world, rank)
+    workers = max(1, (os.cpu_count() or 1) // world)
+    t0 = time.perf_counter()
+    nn_rows = find_ordered_neighbor_rows(locs, args.m, i0, i1 - i0, workers=workers)
+    t_nn = time.perf_counter() - t0
+
+    # pinned host copies (the e2e leg copies from these every step)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hy, hX, hl, hn = pin(y), pin(X), pin(locs), pin(nn_rows)
+    ds = vg.Dataset(hy.numpy(), hX.numpy(), hl.numpy())
+    table = vg.NeighborArray(hn.numpy())  # this rank's rows only
+
+    def new_problem():
+        return engine.DeviceProblem(ds, table, args.family, device=device, row0=i0, rows=i1 - i0, layout=args.layout,
+                                     nn_is_shard=True)
+
+    def step(prob):
+        vec = prob.totals_async(theta)
+        totals, first = distributed.combine_partials(vec)   # all-reduce (N>1) + D2H of L+2 doubles
+        if first >= 0:
+            raise vg.NotPositiveDefinite(pivot=-1, observation=first)
+        return totals
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    prob = new_problem()
+    prob.use_current_stream()
+    prob.enable_timing(True)
+    for _ in range(max(args.warmup, 3)):
+        totals = step(prob)
+    kernel_ms = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        start.record()
+        for _ in range(args.steps):
+            totals = step(prob)
+            kernel_ms.append(prob.last_kernel_ms())
+        end.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = start.elapsed_time(end)
+    launches = args.steps * prob.last_launch_count
+    kernel_name = prob.last_kernel_name
+    layout_used = prob.layout_for(q)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t)
+    ms_per_step = ms_total / args.steps
+    value = n_total / (ms_per_step * 1e-3)
+    ev = vg.assemble(engine.parts_from_flat(totals, args.p, q), n_total)
+    prob.close()
+
+    # ---- end to end: pinned host arrays -> device -> evaluation -> host totals, every step ----
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        with new_problem() as pr:
+            step(pr)
+    barrier()
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    es.record()
+    for _ in range(e2e_steps):
+        with new_problem() as pr:
+            step(pr)
+    ee.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max(es.elapsed_time(ee), 1000.0 * (time.perf_counter() - t0)) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t)
+    h2d = int(hy.numel() * 8 + hX.numel() * 8 + hl.numel() * 8 + hn.numel() * 8)
+    d2h = int((engine.acc_len(args.p, q) + 2) * 8)
+
+    # ---- roofline of the main kernel (FP64 DFMA bound; measured peak) ----
+    burst, sustained = np.zeros(1), np.zeros(1)
+    dp = lambda a: a.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_double))
+    _cabi.check(_cabi.load().vb200_measure_fp64_peak(local_rank, 0.5, dp(burst), dp(sustained)), "fp64 peak")
+    F = algorithmic_flops(args.family, args.d, args.p, q, args.m)
+    k_ms = float(np.mean(kernel_ms))
+    achieved = F["F_min"] * (i1 - i0) / (k_ms * 1e-3) * 1e-12
+    traffic = None
+    tfile = ROOT / "profiles" / "roofline_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(kernel_name)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": float(sustained[0]), "unit": "TFLOP/s",
+                "frac": achieved / float(sustained[0]), "traffic": traffic, "kernel": kernel_name, "layout": layout_used,
+                "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms_per_step,
+                "flops_per_obs": F["F_min"], "flops_per_obs_generic": F["F_generic"],
+                "peak_source": "measured here: register-resident DFMA micro-kernel, sustained over 0.5 s "
+                               "(burst %.2f TFLOP/s); MEASURED_PEAKS.json has no FP64 entry" % float(burst[0]),
+                "hbm_algorithmic_bytes_per_obs": 8 * (args.d + args.p + 1) + 8 * (args.m + 1),
+                "hbm_frac_of_measured_peak": (8 * (args.d + args.p + 1) + 8 * (args.m + 1)) * (i1 - i0)
+                                             / (k_ms * 1e-3) / 1e9 / _hbm_peak()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, n_total),
+        "clocks": clocks.summary(),
+        "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms, "steps": e2e_steps,
+                "path": "engine.DeviceProblem(pinned host y/X/locs/nn) -> vb200_create -> vb200_eval_async -> host"},
+        "gpu_launches": launches, "roofline": roofline,
+        "loglik": ev.loglik, "neighbor_search_s": t_nn,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, y, X, locs, nn_rows, theta)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _hbm_peak():
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        return 6650.0  # the profiling guide's fallback
+
+
+def cpu_baseline(args, y, X, locs, nn_rows, theta):
+    """The oracle port timed on the host cores over a bounded sample (about 10-20 s of CPU work)."""
+    from oracle import reference_core
+    cores = os.cpu_count() or 1
+    probe = 1 << 14
+    row0 = args.n // 2
+    t = cpu_time_oracle(y, X, locs, nn_rows[row0:row0 + probe], row0, args.family, theta, probe, cores)
+    sample = int(min(args.n - row0, max(probe, (probe / t) * 8.0)))
+    sample = 1 << int(np.floor(np.log2(sample)))
+    best = cpu_time_oracle(y, X, locs, nn_rows[row0:row0 + sample], row0, args.family, theta, sample, cores, repeats=2)
+    out = {"value": sample / best, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"rows [{row0}, {row0 + sample}) of the same workload, best of 2 "
+                     f"(C/OpenMP port with the Matern 3/2 pair term; the reference has no Matern family)"}
+    if reference_core.available() and args.n <= (1 << 21):
+        n = y.shape[0]
+        K = reference_core.module()
+        pp, q = args.p, 3
+        slots = (np.zeros(n), np.zeros(n), np.zeros((n, pp, pp)), np.zeros((n, pp)), np.zeros((n, q)), np.zeros((n, q)),
+                 np.zeros((n, pp, q)), np.zeros((n, pp, pp, q)), np.zeros((n, q, q)))
+        failv = np.zeros(n, dtype=np.int32)
+        th = np.array([theta[0], theta[1], theta[-1]])
+        full = np.full((n, args.m + 1), -1, dtype=np.int64)
+        full[row0:row0 + sample] = nn_rows[row0:row0 + sample]
+        bt = float("inf")
+        for _ in range(2):
+            t1 = time.perf_counter()
+            K.RUNNERS["task"](y, X, locs, full, th, 0, 0.0, slots, failv, row0, row0 + sample, cores, 32)
+            bt = min(bt, time.perf_counter() - t1)
+        out["reference_compiled_core_exp_iso_obs_per_s"] = sample / bt
+        out["reference_note"] = ("oracle/_ref = the reference's own compiled core (run_task), exponential_isotropic "
+                                 "kernel on the same rows")
+    return out
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=1 << 20, help="observations per GPU")
+    ap.add_argument("--m", type=int, default=30)
+    ap.add_argument("--d", type=int, default=2)
+    ap.add_argument("--p", type=int, default=1)
+    ap.add_argument("--family", default="matern15_isotropic")
+    ap.add_argument("--theta", type=float, nargs="+", default=[1.0, 0.05, 0.1])
+    ap.add_argument("--layout", default="auto", choices=("auto", "warp_smem", "tiled_reg", "thread_smem"))
+    ap.add_argument("--ref-seconds", type=float, default=2.0, help="target CPU seconds per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

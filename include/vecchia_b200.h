@@ -1,0 +1,164 @@
+/*
+ * vecchia_b200.h -- C ABI of the B200 (sm_100a) Vecchia likelihood core.
+ *
+ * This is the drop-in boundary for ONE path of the reference package
+ * (`vecchiagp`, /root/reference/pkg/src/vecchiagp): the per-observation hot
+ * loop behind `engine.run`.  Every entry point below replaces a piece of the
+ * reference's runner seam; file:line citations are relative to
+ * /root/reference/pkg/src/vecchiagp/.
+ *
+ *   reference interface                                   replaced by
+ *   ----------------------------------------------------  -----------------------
+ *   RUNNERS[backend](y, X, locs_work, nn_idx, theta,      vb200_create (inputs, once)
+ *       kcode, jitter, slots, fail, i0, i1, workers, cap)  + vb200_eval / vb200_eval_async
+ *       engine/__init__.py:237-245, _kernels.pyx:412-429     (theta, jitter, [i0,i1))
+ *   _alloc_slots + _reduce (n-leading slots, host sum)     in-kernel fixed-order reduction;
+ *       engine/__init__.py:141-170                           the L totals come back directly
+ *   fail[i] = pivot+1, lowest failing index wins           first_fail / pivot out-parameters
+ *       _kernels.pyx:384-386,427-429; __init__.py:246-247
+ *   kernel_code 0/1 (covariance.py:33-35)                  vb200_family codes below
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / C++ types cross this boundary;
+ *   - array layouts are the reference's: y (n,), X (n,p) C-order, locs (n,d)
+ *     C-order (already in working coordinates, i.e. after
+ *     CovarianceFamily.prepare_locs, covariance.py:143-152), nn int64
+ *     (rows, m+1) with -1 padding, column 0 = the observation itself
+ *     (preprocess.py:95-118);
+ *   - the accumulator vector has L = (1+q)(2+p+p^2) + q^2 doubles in the
+ *     C order of the reference's slot arrays (engine/__init__.py:141-152):
+ *     logdet, ysy, xsx[p][p], ysx[p], dlogdet[q], dysy[q], dysx[p][q],
+ *     dxsx[p][p][q], ainfo[q][q];
+ *   - every function returns 0 on success or a negative VB200_E* code;
+ *     vb200_last_error() gives the message for the calling thread;
+ *   - a numerically failed factorization is DATA, not an error: the call
+ *     returns 0 with *first_fail = lowest failing observation index and
+ *     *pivot = zero-based failing pivot IN THE REFERENCE'S LOCAL FRAME; the sums
+ *     are then unspecified (the reference returns none either);
+ *   - there is no CPU fallback: without a CUDA device every compute entry point
+ *     fails with VB200_ECUDA.
+ */
+#ifndef VECCHIA_B200_H
+#define VECCHIA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VB200_ABI_VERSION 1
+
+/* error codes */
+#define VB200_OK 0
+#define VB200_EINVAL (-1)   /* bad argument (shape, family, theta arity, range) */
+#define VB200_ECUDA (-2)    /* CUDA runtime error / no device */
+#define VB200_ENOMEM (-3)   /* device or host allocation failed */
+#define VB200_EUNSUPPORTED (-4) /* shape exceeds what the kernels support (m+1 too wide) */
+
+/* covariance families.  Codes 0/1 are the reference's kernel codes
+ * (covariance.py:33-35); the rest are extensions. theta layout:
+ *   EXP_ISO / MATERN15 / MATERN25 : [variance, range, nugget]              (q = 3)
+ *   EXP_ANISO                     : [variance, range_1..range_d, nugget]   (q = d+2)
+ *   EXP_SPACETIME                 : [variance, range_space, range_time, nugget] (q = 4),
+ *                                   time is the LAST coordinate
+ * The nugget is relative: diag = variance*(1+nugget) + jitter (_kernels.pyx:34-50). */
+enum vb200_family {
+    VB200_EXP_ISO = 0,
+    VB200_EXP_ANISO = 1,
+    VB200_EXP_SPACETIME = 2,
+    VB200_MATERN15 = 3,
+    VB200_MATERN25 = 4
+};
+
+/* kernel layouts (the north-star layout study); AUTO picks the fastest that supports the shape */
+enum vb200_layout {
+    VB200_LAYOUT_AUTO = 0,
+    VB200_LAYOUT_WARP_SMEM = 1,   /* warp per observation, matrices in shared memory (any shape) */
+    VB200_LAYOUT_TILED_REG = 2,   /* sub-warp lane groups, rows register-resident (m+1 <= 64) */
+    VB200_LAYOUT_THREAD_SMEM = 3  /* thread per observation, packed triangle in shared memory */
+};
+
+typedef struct vb200_problem vb200_problem; /* opaque: device-resident inputs of one dataset shard */
+
+/* ---- introspection (no device needed) ---------------------------------- */
+int vb200_abi_version(void);
+const char *vb200_last_error(void);
+int vb200_acc_len(int p, int q);             /* L */
+int vb200_family_nparms(int family, int d);  /* q, or VB200_EINVAL */
+int vb200_device_count(void);                /* 0 when no usable CUDA device */
+
+/* ---- problem lifetime --------------------------------------------------- */
+/*
+ * Upload (or adopt) the inputs of one shard.  `nn` holds rows
+ * [nn_row0, nn_row0 + nn_rows) of the neighbor table; y / X / locs always hold
+ * all n points (row i only references indices <= i, preprocess.py:99-101).
+ * Each of y, X, locs, nn may be a HOST pointer (copied to the device here) or
+ * a DEVICE pointer on `device` (adopted without a copy; the caller keeps it
+ * alive until vb200_destroy -- this is how torch-allocated buffers are passed).
+ * `stream` is a cudaStream_t (NULL = a private non-blocking stream).
+ * Replaces the array arguments of the reference runners (_kernels.pyx:392-393).
+ */
+int vb200_create(int device, int64_t n, int p, int d, int mp1,
+                 const double *y, const double *X, const double *locs,
+                 const int64_t *nn, int64_t nn_row0, int64_t nn_rows,
+                 void *stream, vb200_problem **out);
+int vb200_destroy(vb200_problem *prob);
+int vb200_set_stream(vb200_problem *prob, void *stream);
+int vb200_set_layout(vb200_problem *prob, int layout);
+int vb200_get_layout(const vb200_problem *prob, int family, int q); /* layout AUTO resolves to */
+
+/* ---- evaluation --------------------------------------------------------- */
+/*
+ * Totals of the L accumulators over observations [i0, i1) (which must lie in
+ * the shard's nn rows), written to HOST memory; synchronises the stream.
+ * Rows with fewer than m+1 live entries are processed with their true size
+ * (engine/__init__.py:236-239).  Replaces run_sequential + RUNNERS[backend] +
+ * _reduce (engine/__init__.py:233-248).
+ */
+int vb200_eval(vb200_problem *prob, int family, const double *theta, int q, double jitter,
+               int64_t i0, int64_t i1, double *out_sums, int64_t *first_fail, int32_t *pivot);
+
+/*
+ * Asynchronous form for multi-GPU use: enqueues the evaluation on the problem's
+ * stream and leaves L+2 doubles in DEVICE memory at d_out:
+ *   d_out[0..L)  totals,
+ *   d_out[L]     number of failed observations (0.0 on success),
+ *   d_out[L+1]   -(lowest failing index) - 1 when any failed, else -inf  (so a
+ *                MAX all-reduce of this slot, or of the whole vector's last slot,
+ *                yields the globally lowest failing index).
+ * The [0..L] prefix is combined across ranks with one SUM all-reduce.
+ * vb200_fail_info returns the local first failure and its pivot (synchronises).
+ */
+int vb200_eval_async(vb200_problem *prob, int family, const double *theta, int q, double jitter,
+                     int64_t i0, int64_t i1, double *d_out);
+int vb200_sync(vb200_problem *prob);
+int vb200_fail_info(vb200_problem *prob, int64_t *first_fail, int32_t *pivot);
+
+/* per-observation rows (i1-i0, L) into DEVICE or HOST memory -- the analogue of the
+ * reference's slot arrays, for tests and diagnostics (engine/__init__.py:141-152). */
+int vb200_eval_rows(vb200_problem *prob, int family, const double *theta, int q, double jitter,
+                    int64_t i0, int64_t i1, double *rows_host, int32_t *fail_host);
+
+/* number of kernel launches the last vb200_eval* call enqueued, and the name of the
+ * main kernel variant (for bench.py's gpu_launches / roofline bookkeeping) */
+int vb200_last_launch_count(const vb200_problem *prob);
+const char *vb200_last_kernel_name(const vb200_problem *prob);
+
+/* CUDA-event timing of the MAIN kernel only (not the reset / reduction launches): enable,
+ * evaluate, then read the duration of the last main-kernel launch in milliseconds
+ * (synchronises on the closing event).  Used by bench.py for roofline.achieved. */
+int vb200_enable_timing(vb200_problem *prob, int on);
+int vb200_last_kernel_ms(vb200_problem *prob, double *ms);
+
+/* ---- measurement helper -------------------------------------------------- */
+/* FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA) from a register-resident
+ * DFMA micro-kernel timed with CUDA events for about `seconds`: *burst = best single
+ * launch, *sustained = all launches / total time.  MEASURED_PEAKS.json has no FP64
+ * entry, so bench.py measures the roofline denominator itself. */
+int vb200_measure_fp64_peak(int device, double seconds, double *burst_tflops, double *sustained_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VECCHIA_B200_H */

@@ -1,0 +1,151 @@
+// common.cuh -- shared device-side definitions of the B200 Vecchia core.
+//
+// Reference map (paths relative to /root/reference/pkg/src/vecchiagp):
+//   PairTerms / pair_terms   <- engine/_kernels.pyx:34-99 (_cov_entry, _dcov_entry), evaluated ONCE per
+//                               pair instead of once per (parameter, pair) as the reference does
+//   accumulator layout       <- engine/__init__.py:141-152 (_alloc_slots order)
+//   emit_value               <- engine/_kernels.pyx:294-344 (_contract)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define VB_MAXD 20            // coordinates per point
+#define VB_MAXQ (VB_MAXD + 2) // covariance parameters
+#define VB_MAXP 16            // design columns
+
+enum : int { FAM_EXP_ISO = 0, FAM_EXP_ANISO = 1, FAM_EXP_SPACETIME = 2, FAM_MATERN15 = 3, FAM_MATERN25 = 4 };
+
+// Everything one evaluation needs, passed by value as the kernel argument.
+struct EvalParams {
+    const double *rec;      // packed point records, rs doubles each: locs[d], y, X[p], (pad)
+    const int64_t *nn;      // neighbor rows of this shard, (nn_rows, mp1), -1 padded
+    int64_t nn_row0;        // global index of the first row held in nn
+    int64_t i0, i1;         // observation range of this evaluation
+    int p, d, q, mp1, rs, family;
+    int qd;                 // number of range-like ("dense") parameters = q - 2
+    int L;                  // accumulator length
+    double sig2, tau2, jitter, diag; // diag = sig2*(1+tau2) + jitter
+    double inv_sig2;
+    double inv_rho[VB_MAXD]; // per-axis inverse ranges (iso: all equal; space-time: space,..,space,time)
+    double *partials;        // [gridDim.x][L] block partial sums
+    unsigned long long *fail_word; // min over failures of (index << 16 | pivot+1)
+    unsigned int *fail_count;
+    double *rows;            // optional (i1-i0, L) per-observation output (diagnostics); nullptr normally
+    int *fail_rows;          // optional (i1-i0) pivot+1 per observation
+    int ws_doubles;          // per-warp scratch doubles (warp_smem layout)
+};
+
+// Covariance and range-derivative values of one off-diagonal pair.
+//   dl[l] = pa[l] - pc[l] is supplied by the caller (coordinates in the working frame).
+// Families follow include/vecchia_b200.h.  Dv has qd entries.
+template <int FAM>
+__device__ __forceinline__ void pair_terms(const EvalParams &P, const double *dl, double &Kv, double *Dv)
+{
+    if (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
+        double d2 = 0.0;
+        for (int l = 0; l < P.d; ++l)
+            d2 = fma(dl[l], dl[l], d2);
+        const double ir = P.inv_rho[0];
+        const double x = sqrt(d2) * ir;
+        const double e = exp(-x);
+        if (FAM == FAM_EXP_ISO) {
+            Kv = P.sig2 * e;             // sigma^2 exp(-r/rho)            (_kernels.pyx:44-46)
+            Dv[0] = Kv * x * ir;         // sigma^2 exp(-r/rho) r / rho^2  (_kernels.pyx:70-76)
+        } else if (FAM == FAM_MATERN15) {
+            const double se = P.sig2 * e;
+            Kv = se * (1.0 + x);
+            Dv[0] = se * x * x * ir;
+        } else {
+            const double se = P.sig2 * e;
+            Kv = se * (1.0 + x + x * x * (1.0 / 3.0));
+            Dv[0] = se * x * x * (1.0 + x) * ir * (1.0 / 3.0);
+        }
+    } else {
+        // anisotropic / space-time: s = || delta / rho ||              (_kernels.pyx:47-50, 78-99)
+        double s2 = 0.0, sp2 = 0.0;
+        double sc[VB_MAXD];
+        for (int l = 0; l < P.d; ++l) {
+            sc[l] = dl[l] * P.inv_rho[l];
+            sc[l] *= sc[l];
+            s2 += sc[l];
+            if (l < P.d - 1)
+                sp2 += sc[l];
+        }
+        const double s = sqrt(s2);
+        Kv = P.sig2 * exp(-s);
+        const double g = (s == 0.0) ? 0.0 : Kv / s;
+        if (FAM == FAM_EXP_ANISO) {
+            for (int l = 0; l < P.d; ++l)
+                Dv[l] = g * sc[l] * P.inv_rho[l];
+        } else {
+            Dv[0] = g * sp2 * P.inv_rho[0];
+            Dv[1] = g * sc[P.d - 1] * P.inv_rho[P.d - 1];
+        }
+    }
+}
+
+// Accumulator offsets for given (p, q).
+struct AccLayout {
+    int xsx, ysx, dlogdet, dysy, dysx, dxsx, ainfo, L;
+    __host__ __device__ AccLayout(int p, int q)
+    {
+        xsx = 2;
+        ysx = xsx + p * p;
+        dlogdet = ysx + p;
+        dysy = dlogdet + q;
+        dysx = dysy + q;
+        dxsx = dysx + p * q;
+        ainfo = dxsx + p * p * q;
+        L = ainfo + q * q;
+    }
+};
+
+// Value of accumulator entry o for one observation, from the per-observation
+// scalars (restates _contract, _kernels.pyx:294-344):
+//   logdet, ze = z_e, we[b] = W_eb, ce[j] = c_je, zc[j] = z.c_j,
+//   wc[b*q+j] = (W^T c_j)_b, cc[j*q+l] = c_j.c_l
+__device__ __forceinline__ double emit_value(int o, int p, int q, const AccLayout &A, double logdet, double ze,
+                                             const double *we, const double *ce, const double *zc,
+                                             const double *wc, const double *cc)
+{
+    if (o == 0)
+        return logdet;
+    if (o == 1)
+        return ze * ze;
+    if (o < A.ysx) {
+        const int t = o - A.xsx, a = t / p, b = t - a * p;
+        return we[a] * we[b];
+    }
+    if (o < A.dlogdet)
+        return ze * we[o - A.ysx];
+    if (o < A.dysy)
+        return ce[o - A.dlogdet];
+    if (o < A.dysx) {
+        const int j = o - A.dysy;
+        return ce[j] * ze * ze - 2.0 * ze * zc[j];
+    }
+    if (o < A.dxsx) {
+        const int t = o - A.dysx, b = t / q, j = t - b * q;
+        return ce[j] * ze * we[b] - ze * wc[b * q + j] - zc[j] * we[b];
+    }
+    if (o < A.ainfo) {
+        const int t = o - A.dxsx, ab = t / q, j = t - ab * q, a = ab / p, b = ab - a * p;
+        return ce[j] * we[a] * we[b] - wc[a * q + j] * we[b] - we[a] * wc[b * q + j];
+    }
+    const int t = o - A.ainfo, j = t / q, l = t - j * q;
+    return cc[j * q + l] - 0.5 * ce[j] * ce[l];
+}
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+__device__ __forceinline__ void report_failure(const EvalParams &P, int64_t i, int pivot_plus1)
+{
+    atomicMin(P.fail_word, ((unsigned long long)i << 16) | (unsigned long long)(pivot_plus1 & 0xffff));
+    atomicAdd(P.fail_count, 1u);
+}

@@ -1,0 +1,308 @@
+// host_neighbors.cpp -- host-side ordered nearest-predecessor search (C ABI, OpenMP).
+//
+// The neighbor table is an INPUT of the GPU path and stays on the host (BASELINE.json
+// north_star); it must equal the reference's table entry for entry.  The reference
+// defines it by an exhaustive scan (/root/reference/pkg/src/vecchiagp/engine/
+// _kernels.pyx:609-651, preprocess.py:121-132): row i = i followed by the m
+// predecessors j < i with the smallest (d2, j) in lexicographic order, where
+// d2 = sum over axes of (x_i - x_j)^2 accumulated left to right in double precision
+// WITHOUT fused multiply-add (pkg/setup.py:18-25).  That scan is O(n^2) -- hours at
+// n >= 2^22 -- so this file provides the same table from a multi-resolution uniform
+// grid: candidates are enumerated ring by ring around the query cell and ranked with
+// the identical d2 expression and tie rule, and the search stops only when no
+// unvisited cell can hold a point that beats or ties the current m-th best.
+// Build with -ffp-contract=off (see build.py) so d2 is bit-identical.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+struct Cand {
+    double d2;
+    int64_t j;
+};
+
+inline bool before(double d2a, int64_t ja, double d2b, int64_t jb) { return d2a < d2b || (d2a == d2b && ja < jb); }
+
+// bounded sorted list of the m best (d2, j) keys
+struct Best {
+    Cand *v;
+    int m, cnt;
+    inline double worst() const { return v[m - 1].d2; }
+    inline int64_t worst_j() const { return v[m - 1].j; }
+    inline void offer(double d2, int64_t j)
+    {
+        if (cnt == m && !before(d2, j, v[m - 1].d2, v[m - 1].j))
+            return;
+        int pos = cnt < m ? cnt++ : m - 1;
+        while (pos > 0 && before(d2, j, v[pos - 1].d2, v[pos - 1].j)) {
+            v[pos] = v[pos - 1];
+            --pos;
+        }
+        v[pos].d2 = d2;
+        v[pos].j = j;
+    }
+};
+
+inline double sqdist(const double *a, const double *b, int d)
+{
+    double s = 0.0;
+    for (int l = 0; l < d; ++l) {
+        const double diff = a[l] - b[l];
+        s += diff * diff;
+    }
+    return s;
+}
+
+// One grid level: the first `count` points binned on the first g axes.
+struct Level {
+    int64_t count = 0;
+    int g = 0;
+    int dims[3] = {1, 1, 1};
+    double h = 1.0, inv_h = 1.0;
+    std::vector<int64_t> start; // cell -> first slot
+    std::vector<int32_t> items; // point indices, ascending inside a cell
+};
+
+struct Grid {
+    int g;
+    double lo[3], ext[3];
+    std::vector<Level> levels;
+    std::vector<int64_t> level_count;
+};
+
+inline void cell_of(const Level &L, const Grid &G, const double *x, int *c)
+{
+    for (int a = 0; a < 3; ++a) {
+        if (a < L.g) {
+            int v = (int)std::floor((x[a] - G.lo[a]) * L.inv_h);
+            c[a] = v < 0 ? 0 : (v >= L.dims[a] ? L.dims[a] - 1 : v);
+        } else {
+            c[a] = 0;
+        }
+    }
+}
+
+void build_level(Level &L, const Grid &G, const double *locs, int d, int64_t count, double per_cell)
+{
+    L.count = count;
+    L.g = G.g;
+    double vol = 1.0;
+    int live = 0;
+    for (int a = 0; a < G.g; ++a)
+        if (G.ext[a] > 0.0) {
+            vol *= G.ext[a];
+            ++live;
+        }
+    double h = live ? std::pow(vol * per_cell / (double)count, 1.0 / live) : 1.0;
+    if (!(h > 0.0) || !std::isfinite(h))
+        h = 1.0;
+    // cap the number of cells
+    for (;;) {
+        double cells = 1.0;
+        for (int a = 0; a < G.g; ++a)
+            cells *= std::floor(G.ext[a] / h) + 1.0;
+        if (cells <= 4.0 * (double)count + 64.0)
+            break;
+        h *= 1.5;
+    }
+    L.h = h;
+    L.inv_h = 1.0 / h;
+    int64_t ncell = 1;
+    for (int a = 0; a < 3; ++a) {
+        L.dims[a] = a < G.g ? (int)std::floor(G.ext[a] / h) + 1 : 1;
+        ncell *= L.dims[a];
+    }
+    L.start.assign((size_t)ncell + 1, 0);
+    std::vector<int64_t> cid((size_t)count);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < count; ++i) {
+        int c[3];
+        cell_of(L, G, locs + i * d, c);
+        cid[i] = ((int64_t)c[2] * L.dims[1] + c[1]) * L.dims[0] + c[0];
+    }
+    for (int64_t i = 0; i < count; ++i)
+        L.start[cid[i] + 1]++;
+    for (int64_t c = 0; c < ncell; ++c)
+        L.start[c + 1] += L.start[c];
+    L.items.resize((size_t)count);
+    std::vector<int64_t> fill(L.start.begin(), L.start.end() - 1);
+    for (int64_t i = 0; i < count; ++i) // ascending i keeps each cell sorted by index
+        L.items[fill[cid[i]]++] = (int32_t)i;
+}
+
+void exhaustive_row(const double *locs, int d, int64_t i, Best &B)
+{
+    const double *xi = locs + i * d;
+    for (int64_t j = 0; j < i; ++j)
+        B.offer(sqdist(xi, locs + j * d, d), j);
+}
+
+void grid_row(const Grid &G, const Level &L, const double *locs, int d, int64_t i, Best &B)
+{
+    const double *xi = locs + i * d;
+    int cq[3];
+    cell_of(L, G, xi, cq);
+    int maxr = 0;
+    for (int a = 0; a < L.g; ++a)
+        maxr = std::max(maxr, std::max(cq[a], L.dims[a] - 1 - cq[a]));
+    for (int r = 0; r <= maxr; ++r) {
+        if (r >= 1 && B.cnt == B.m) {
+            // every unvisited cell is at least r cells away along some axis: its points are
+            // farther than (r-1)*h + (distance to the own cell face) >= (r-1)*h ... use the
+            // conservative bound with a relative safety margin for the floor() rounding.
+            const double lb = (double)(r - 1) * L.h * 0.999999;
+            if (r >= 2 && B.worst() < lb * lb)
+                break;
+        }
+        const int z0 = L.g > 2 ? std::max(cq[2] - r, 0) : 0, z1 = L.g > 2 ? std::min(cq[2] + r, L.dims[2] - 1) : 0;
+        const int y0 = L.g > 1 ? std::max(cq[1] - r, 0) : 0, y1 = L.g > 1 ? std::min(cq[1] + r, L.dims[1] - 1) : 0;
+        const int x0 = std::max(cq[0] - r, 0), x1 = std::min(cq[0] + r, L.dims[0] - 1);
+        for (int z = z0; z <= z1; ++z) {
+            const bool zface = L.g > 2 && (z == cq[2] - r || z == cq[2] + r);
+            for (int y = y0; y <= y1; ++y) {
+                const bool yface = L.g > 1 && (y == cq[1] - r || y == cq[1] + r);
+                const int64_t rowbase = ((int64_t)z * L.dims[1] + y) * L.dims[0];
+                if (zface || yface) {
+                    // whole x-run belongs to the shell
+                    const int64_t s = L.start[rowbase + x0], e = L.start[rowbase + x1 + 1];
+                    for (int64_t t = s; t < e; ++t) {
+                        const int64_t j = L.items[t];
+                        if (j >= i)
+                            continue;
+                        B.offer(sqdist(xi, locs + j * d, d), j);
+                    }
+                } else {
+                    // only the two x faces
+                    for (int side = 0; side < 2; ++side) {
+                        const int x = side ? cq[0] + r : cq[0] - r;
+                        if (x < 0 || x >= L.dims[0] || (side && r == 0))
+                            continue;
+                        const int64_t s = L.start[rowbase + x], e = L.start[rowbase + x + 1];
+                        for (int64_t t = s; t < e; ++t) {
+                            const int64_t j = L.items[t];
+                            if (j >= i)
+                                continue;
+                            B.offer(sqdist(xi, locs + j * d, d), j);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int vbh_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+// Exhaustive scan (the normative algorithm).  out is (n, m+1) int64.
+int vbh_neighbors_exhaustive(const double *locs, int64_t n, int d, int m, int workers, int64_t *out)
+{
+    if (!locs || !out || n < 1 || d < 1 || m < 1)
+        return -1;
+    if (workers < 1)
+        workers = 1;
+#pragma omp parallel num_threads(workers)
+    {
+        std::vector<Cand> buf((size_t)m);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            Best B{buf.data(), m, 0};
+            exhaustive_row(locs, d, i, B);
+            int64_t *row = out + i * (m + 1);
+            row[0] = i;
+            for (int t = 0; t < m; ++t)
+                row[1 + t] = t < B.cnt ? B.v[t].j : -1;
+        }
+    }
+    return 0;
+}
+
+// Grid-accelerated search of rows [row0, row0 + rows) only; out is (rows, m+1).  Identical
+// output to the corresponding rows of vbh_neighbors_exhaustive.  Each rank of a multi-GPU
+// run builds just its own shard of the table with this entry point.
+int vbh_neighbors_grid_rows(const double *locs, int64_t n, int d, int m, int workers, int64_t row0, int64_t rows,
+                            int64_t *out)
+{
+    if (!locs || !out || n < 1 || d < 1 || m < 1 || row0 < 0 || rows < 0 || row0 + rows > n)
+        return -1;
+    if (n > (int64_t)0x7fffffff)
+        return -2;
+    if (workers < 1)
+        workers = 1;
+    for (int64_t t = 0; t < n * d; ++t)
+        if (!std::isfinite(locs[t]))
+            return -3;
+    Grid G;
+    G.g = d < 3 ? d : 3;
+    for (int a = 0; a < G.g; ++a) {
+        double lo = locs[a], hi = locs[a];
+        for (int64_t i = 1; i < n; ++i) {
+            const double v = locs[i * d + a];
+            lo = v < lo ? v : lo;
+            hi = v > hi ? v : hi;
+        }
+        G.lo[a] = lo;
+        G.ext[a] = hi - lo;
+    }
+    // levels cover prefixes of length base * 2^l; rows below `base` are scanned exhaustively
+    const int64_t base = std::max<int64_t>(1024, 16 * (int64_t)m);
+    const double per_cell = std::max(3.0, 0.35 * m);
+    for (int64_t c = 2 * base; ; c *= 2) {
+        const int64_t cnt = std::min(c, n);
+        if (cnt <= base)
+            break;
+        G.level_count.push_back(cnt);
+        if (cnt == n)
+            break;
+    }
+    G.levels.resize(G.level_count.size());
+    for (size_t l = 0; l < G.levels.size(); ++l)
+        build_level(G.levels[l], G, locs, d, G.level_count[l], per_cell);
+#pragma omp parallel num_threads(workers)
+    {
+        std::vector<Cand> buf((size_t)m);
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t i = row0; i < row0 + rows; ++i) {
+            Best B{buf.data(), m, 0};
+            if (i <= base || G.levels.empty()) {
+                exhaustive_row(locs, d, i, B);
+            } else {
+                size_t l = 0;
+                while (G.level_count[l] < i)
+                    ++l;
+                grid_row(G, G.levels[l], locs, d, i, B);
+            }
+            int64_t *row = out + (i - row0) * (m + 1);
+            row[0] = i;
+            for (int t = 0; t < m; ++t)
+                row[1 + t] = t < B.cnt ? B.v[t].j : -1;
+        }
+    }
+    return 0;
+}
+
+// Grid-accelerated search of the whole table; identical output to vbh_neighbors_exhaustive.
+int vbh_neighbors_grid(const double *locs, int64_t n, int d, int m, int workers, int64_t *out)
+{
+    return vbh_neighbors_grid_rows(locs, n, d, m, workers, 0, n, out);
+}
+
+} // extern "C"

@@ -1,0 +1,710 @@
+// vecchia_b200.cu -- C ABI (include/vecchia_b200.h) over the sm_100a kernels.
+// Host side: problem lifetime, launch configuration, fixed-order reduction, failure report.
+#include "../../include/vecchia_b200.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "common.cuh"
+#include "kernel_warp_smem.cuh"
+#include "kernel_tiled.cuh"
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                                   \
+    do {                                                                                                 \
+        cudaError_t _e = (expr);                                                                         \
+        if (_e != cudaSuccess)                                                                           \
+            return fail(_e == cudaErrorMemoryAllocation ? VB200_ENOMEM : VB200_ECUDA,                    \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));                             \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+// Pack y / X / locs (reference row-major arrays) into one record per point:
+// rec[i] = { locs[i][0..d), y[i], X[i][0..p), pad } -- one gather touches one or two
+// 32-byte sectors instead of d+p+1 separate arrays.
+__global__ void pack_records_kernel(const double *y, const double *X, const double *locs, int64_t n, int p, int d,
+                                    int rs, double *rec)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    double *r = rec + i * rs;
+    for (int l = 0; l < d; ++l)
+        r[l] = locs[i * d + l];
+    r[d] = y[i];
+    for (int b = 0; b < p; ++b)
+        r[d + 1 + b] = X[i * p + b];
+    for (int t = d + 1 + p; t < rs; ++t)
+        r[t] = 0.0;
+}
+
+// Fixed-order reduction of the block partials: thread o adds column o of
+// partials[nblocks][L] as a pairwise tree over a power-of-two padded index range,
+// so the result does not depend on scheduling (run-to-run reproducible).
+__global__ void reduce_partials_kernel(const double *partials, int nblocks, int L, double *out,
+                                       const unsigned long long *fail_word, const unsigned int *fail_count)
+{
+    extern __shared__ double red[];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int o = 0; o < L; ++o) {
+        double s = 0.0;
+        for (int b = tid; b < nblocks; b += nt)
+            s += partials[(size_t)b * L + o];
+        red[tid] = s;
+        __syncthreads();
+        for (int off = nt >> 1; off > 0; off >>= 1) {
+            if (tid < off)
+                red[tid] += red[tid + off];
+            __syncthreads();
+        }
+        if (tid == 0)
+            out[o] = red[0];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const unsigned int cnt = *fail_count;
+        out[L] = (double)cnt;
+        out[L + 1] = cnt ? -(double)((*fail_word) >> 16) - 1.0 : -INFINITY;
+    }
+}
+
+__global__ void reset_fail_kernel(unsigned long long *fail_word, unsigned int *fail_count)
+{
+    *fail_word = ~0ull;
+    *fail_count = 0u;
+}
+
+// Register-resident DFMA chains: 16 independent accumulators per thread.
+__global__ void dfma_peak_kernel(double *sink, int iters, double a, double b)
+{
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+           x7 = x0 + 7, x8 = x0 + 8, x9 = x0 + 9, xa = x0 + 10, xb = x0 + 11, xc = x0 + 12, xd = x0 + 13,
+           xe = x0 + 14, xf = x0 + 15;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+            x8 = fma(x8, a, b); x9 = fma(x9, a, b); xa = fma(xa, a, b); xb = fma(xb, a, b);
+            xc = fma(xc, a, b); xd = fma(xd, a, b); xe = fma(xe, a, b); xf = fma(xf, a, b);
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7 + x8 + x9 + xa + xb + xc + xd + xe + xf;
+    if (s == 12345.678)
+        sink[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// problem object
+// ---------------------------------------------------------------------------
+struct vb200_problem {
+    int device = 0;
+    int64_t n = 0;
+    int p = 0, d = 0, mp1 = 0, rs = 0;
+    double *rec = nullptr;
+    const int64_t *nn = nullptr;
+    bool own_nn = false;
+    int64_t nn_row0 = 0, nn_rows = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double *partials = nullptr;
+    size_t partials_cap = 0; // doubles
+    double *d_out = nullptr; // L+2 (own result vector for vb200_eval)
+    size_t d_out_cap = 0;
+    unsigned long long *fail_word = nullptr;
+    unsigned int *fail_count = nullptr;
+    double *h_out = nullptr; // pinned
+    size_t h_out_cap = 0;
+    unsigned long long *h_fail = nullptr; // pinned
+    int layout = VB200_LAYOUT_AUTO;
+    int last_launches = 0;
+    const char *last_kernel = "";
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+static bool is_device_ptr(const void *ptr)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+extern "C" int vb200_abi_version(void) { return VB200_ABI_VERSION; }
+extern "C" const char *vb200_last_error(void) { return g_err.c_str(); }
+extern "C" int vb200_acc_len(int p, int q) { return (1 + q) * (2 + p + p * p) + q * q; }
+
+extern "C" int vb200_family_nparms(int family, int d)
+{
+    switch (family) {
+    case VB200_EXP_ISO:
+    case VB200_MATERN15:
+    case VB200_MATERN25:
+        return 3;
+    case VB200_EXP_ANISO:
+        return d + 2;
+    case VB200_EXP_SPACETIME:
+        return d >= 2 ? 4 : VB200_EINVAL;
+    default:
+        return VB200_EINVAL;
+    }
+}
+
+extern "C" int vb200_device_count(void)
+{
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+extern "C" int vb200_create(int device, int64_t n, int p, int d, int mp1, const double *y, const double *X,
+                            const double *locs, const int64_t *nn, int64_t nn_row0, int64_t nn_rows, void *stream,
+                            vb200_problem **out)
+{
+    if (!out)
+        return fail(VB200_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || p < 1 || d < 1 || mp1 < 1)
+        return fail(VB200_EINVAL, "n, p, d, m+1 must be >= 1");
+    if (p > VB_MAXP || d > VB_MAXD)
+        return fail(VB200_EUNSUPPORTED, "p or d exceeds the compiled limits (p <= 16, d <= 20)");
+    if (mp1 > 0xfff0)
+        return fail(VB200_EUNSUPPORTED, "m+1 too large");
+    if (!y || !X || !locs || !nn)
+        return fail(VB200_EINVAL, "NULL input array");
+    if (nn_row0 < 0 || nn_rows < 0 || nn_row0 + nn_rows > n)
+        return fail(VB200_EINVAL, "neighbor rows outside [0, n)");
+    if (vb200_device_count() <= device || device < 0)
+        return fail(VB200_ECUDA, "no such CUDA device (this library has no CPU fallback)");
+    CUDA_TRY(cudaSetDevice(device));
+
+    vb200_problem *P = new vb200_problem();
+    P->device = device;
+    P->n = n;
+    P->p = p;
+    P->d = d;
+    P->mp1 = mp1;
+    P->rs = (d + 1 + p + 1) & ~1;
+    P->nn_row0 = nn_row0;
+    P->nn_rows = nn_rows;
+    int rc = VB200_OK;
+    double *ty = nullptr, *tX = nullptr, *tl = nullptr;
+    auto cleanup_tmp = [&]() {
+        if (ty) cudaFree(ty);
+        if (tX) cudaFree(tX);
+        if (tl) cudaFree(tl);
+    };
+#define TRY_OR_FREE(expr)                                                                                \
+    do {                                                                                                 \
+        cudaError_t _e = (expr);                                                                         \
+        if (_e != cudaSuccess) {                                                                         \
+            rc = fail(_e == cudaErrorMemoryAllocation ? VB200_ENOMEM : VB200_ECUDA,                      \
+                      std::string(#expr) + ": " + cudaGetErrorString(_e));                               \
+            cleanup_tmp();                                                                               \
+            vb200_destroy(P);                                                                            \
+            return rc;                                                                                   \
+        }                                                                                                \
+    } while (0)
+
+    if (stream) {
+        P->stream = (cudaStream_t)stream;
+    } else {
+        TRY_OR_FREE(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+        P->own_stream = true;
+    }
+    cudaDeviceProp prop;
+    TRY_OR_FREE(cudaGetDeviceProperties(&prop, device));
+    P->sm_count = prop.multiProcessorCount;
+    P->smem_optin = prop.sharedMemPerBlockOptin;
+
+    const double *dy = y, *dX = X, *dl = locs;
+    if (!is_device_ptr(y)) {
+        TRY_OR_FREE(cudaMalloc(&ty, sizeof(double) * n));
+        TRY_OR_FREE(cudaMemcpyAsync(ty, y, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
+        dy = ty;
+    }
+    if (!is_device_ptr(X)) {
+        TRY_OR_FREE(cudaMalloc(&tX, sizeof(double) * n * p));
+        TRY_OR_FREE(cudaMemcpyAsync(tX, X, sizeof(double) * n * p, cudaMemcpyHostToDevice, P->stream));
+        dX = tX;
+    }
+    if (!is_device_ptr(locs)) {
+        TRY_OR_FREE(cudaMalloc(&tl, sizeof(double) * n * d));
+        TRY_OR_FREE(cudaMemcpyAsync(tl, locs, sizeof(double) * n * d, cudaMemcpyHostToDevice, P->stream));
+        dl = tl;
+    }
+    TRY_OR_FREE(cudaMalloc(&P->rec, sizeof(double) * n * P->rs));
+    {
+        const int bs = 256;
+        const unsigned grid = (unsigned)((n + bs - 1) / bs);
+        pack_records_kernel<<<grid, bs, 0, P->stream>>>(dy, dX, dl, n, p, d, P->rs, P->rec);
+        TRY_OR_FREE(cudaGetLastError());
+    }
+    if (is_device_ptr(nn)) {
+        P->nn = nn;
+    } else {
+        int64_t *tn = nullptr;
+        const size_t bytes = sizeof(int64_t) * (size_t)(nn_rows > 0 ? nn_rows : 1) * mp1;
+        TRY_OR_FREE(cudaMalloc(&tn, bytes));
+        P->nn = tn;
+        P->own_nn = true;
+        if (nn_rows > 0)
+            TRY_OR_FREE(cudaMemcpyAsync(tn, nn, sizeof(int64_t) * (size_t)nn_rows * mp1, cudaMemcpyHostToDevice,
+                                        P->stream));
+    }
+    TRY_OR_FREE(cudaMalloc(&P->fail_word, sizeof(unsigned long long)));
+    TRY_OR_FREE(cudaMalloc(&P->fail_count, sizeof(unsigned int)));
+    TRY_OR_FREE(cudaMallocHost(&P->h_fail, sizeof(unsigned long long)));
+    TRY_OR_FREE(cudaStreamSynchronize(P->stream));
+    cleanup_tmp();
+#undef TRY_OR_FREE
+    *out = P;
+    return VB200_OK;
+}
+
+extern "C" int vb200_destroy(vb200_problem *P)
+{
+    if (!P)
+        return VB200_OK;
+    cudaSetDevice(P->device);
+    if (P->stream)
+        cudaStreamSynchronize(P->stream);
+    if (P->rec) cudaFree(P->rec);
+    if (P->own_nn && P->nn) cudaFree((void *)P->nn);
+    if (P->partials) cudaFree(P->partials);
+    if (P->d_out) cudaFree(P->d_out);
+    if (P->fail_word) cudaFree(P->fail_word);
+    if (P->fail_count) cudaFree(P->fail_count);
+    if (P->h_out) cudaFreeHost(P->h_out);
+    if (P->h_fail) cudaFreeHost(P->h_fail);
+    if (P->ev0) cudaEventDestroy(P->ev0);
+    if (P->ev1) cudaEventDestroy(P->ev1);
+    if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
+    cudaGetLastError();
+    delete P;
+    return VB200_OK;
+}
+
+extern "C" int vb200_set_stream(vb200_problem *P, void *stream)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    cudaSetDevice(P->device);
+    if (P->stream)
+        cudaStreamSynchronize(P->stream);
+    if (P->own_stream && P->stream)
+        cudaStreamDestroy(P->stream);
+    P->own_stream = false;
+    P->stream = (cudaStream_t)stream;
+    return VB200_OK;
+}
+
+extern "C" int vb200_set_layout(vb200_problem *P, int layout)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    if (layout < VB200_LAYOUT_AUTO || layout > VB200_LAYOUT_THREAD_SMEM)
+        return fail(VB200_EINVAL, "unknown layout");
+    P->layout = layout;
+    return VB200_OK;
+}
+
+// ---------------------------------------------------------------------------
+// evaluation
+// ---------------------------------------------------------------------------
+static int fill_params(const vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
+                       int64_t i1, EvalParams &E)
+{
+    const int want = vb200_family_nparms(family, P->d);
+    if (want < 0)
+        return fail(VB200_EINVAL, "unknown covariance family code or d too small for it");
+    if (q != want)
+        return fail(VB200_EINVAL, "theta has the wrong length for this family and d");
+    if (!theta)
+        return fail(VB200_EINVAL, "theta is NULL");
+    for (int j = 0; j < q; ++j)
+        if (!std::isfinite(theta[j]))
+            return fail(VB200_EINVAL, "covariance parameters must be finite");
+    for (int j = 0; j + 1 < q; ++j)
+        if (!(theta[j] > 0.0))
+            return fail(VB200_EINVAL, "variance and range parameters must be strictly positive");
+    if (theta[q - 1] < 0.0)
+        return fail(VB200_EINVAL, "nugget must be >= 0");
+    if (i0 < P->nn_row0 || i1 > P->nn_row0 + P->nn_rows || i1 < i0)
+        return fail(VB200_EINVAL, "[i0, i1) outside the neighbor rows of this shard");
+    memset(&E, 0, sizeof(E));
+    E.rec = P->rec;
+    E.nn = P->nn;
+    E.nn_row0 = P->nn_row0;
+    E.i0 = i0;
+    E.i1 = i1;
+    E.p = P->p;
+    E.d = P->d;
+    E.q = q;
+    E.qd = q - 2;
+    E.mp1 = P->mp1;
+    E.rs = P->rs;
+    E.family = family;
+    E.L = vb200_acc_len(P->p, q);
+    E.sig2 = theta[0];
+    E.tau2 = theta[q - 1];
+    E.jitter = jitter;
+    E.diag = theta[0] * (1.0 + theta[q - 1]) + jitter;
+    E.inv_sig2 = 1.0 / theta[0];
+    for (int l = 0; l < P->d; ++l) {
+        double rho;
+        if (family == VB200_EXP_ANISO)
+            rho = theta[1 + l];
+        else if (family == VB200_EXP_SPACETIME)
+            rho = (l < P->d - 1) ? theta[1] : theta[2];
+        else
+            rho = theta[1];
+        E.inv_rho[l] = 1.0 / rho;
+    }
+    E.fail_word = P->fail_word;
+    E.fail_count = P->fail_count;
+    return VB200_OK;
+}
+
+static int ensure_partials(vb200_problem *P, size_t doubles)
+{
+    if (doubles <= P->partials_cap)
+        return VB200_OK;
+    if (P->partials)
+        cudaFree(P->partials);
+    P->partials = nullptr;
+    P->partials_cap = 0;
+    CUDA_TRY(cudaMalloc(&P->partials, sizeof(double) * doubles));
+    P->partials_cap = doubles;
+    return VB200_OK;
+}
+
+typedef void (*ws_kernel_t)(const EvalParams);
+
+static ws_kernel_t ws_kernel_for(int family)
+{
+    switch (family) {
+    case VB200_EXP_ISO: return vecchia_warp_smem_kernel<FAM_EXP_ISO>;
+    case VB200_EXP_ANISO: return vecchia_warp_smem_kernel<FAM_EXP_ANISO>;
+    case VB200_EXP_SPACETIME: return vecchia_warp_smem_kernel<FAM_EXP_SPACETIME>;
+    case VB200_MATERN15: return vecchia_warp_smem_kernel<FAM_MATERN15>;
+    default: return vecchia_warp_smem_kernel<FAM_MATERN25>;
+    }
+}
+
+// Launch the WARP_SMEM layout; returns the number of blocks via *nblocks.
+static int launch_warp_smem(vb200_problem *P, EvalParams &E, int *nblocks)
+{
+    E.ws_doubles = warp_smem_doubles(P->mp1, P->d, P->p, E.q);
+    int warps = WS_WARPS_MAX;
+    while (warps > 1 && (size_t)warps * E.ws_doubles * sizeof(double) > P->smem_optin)
+        warps >>= 1;
+    const size_t smem = (size_t)warps * E.ws_doubles * sizeof(double);
+    if (smem > P->smem_optin)
+        return fail(VB200_EUNSUPPORTED, "m+1 too wide for the shared-memory layout on this device");
+    ws_kernel_t kern = ws_kernel_for(E.family);
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
+    if (per_sm < 1)
+        per_sm = 1;
+    const int64_t count = E.i1 - E.i0;
+    int64_t blocks = (int64_t)P->sm_count * per_sm;
+    const int64_t need = (count + warps - 1) / warps;
+    if (blocks > need)
+        blocks = need;
+    if (blocks < 1)
+        blocks = 1;
+    int rc = ensure_partials(P, (size_t)blocks * E.L);
+    if (rc)
+        return rc;
+    E.partials = P->partials;
+    kern<<<(unsigned)blocks, warps * 32, smem, P->stream>>>(E);
+    CUDA_TRY(cudaGetLastError());
+    *nblocks = (int)blocks;
+    P->last_kernel = "vecchia_warp_smem_kernel";
+    return VB200_OK;
+}
+
+static int resolve_layout(const vb200_problem *P, int family, int q)
+{
+    int layout = P->layout;
+    if (layout == VB200_LAYOUT_AUTO)
+        layout = tiled_supported(family, P->mp1, P->p, P->d, q) ? VB200_LAYOUT_TILED_REG : VB200_LAYOUT_WARP_SMEM;
+    return layout;
+}
+
+extern "C" int vb200_get_layout(const vb200_problem *P, int family, int q)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    return resolve_layout(P, family, q);
+}
+
+static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
+                        int64_t i1, double *d_out, double *d_rows, int *d_fail_rows)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    CUDA_TRY(cudaSetDevice(P->device));
+    EvalParams E;
+    int rc = fill_params(P, family, theta, q, jitter, i0, i1, E);
+    if (rc)
+        return rc;
+    E.rows = d_rows;
+    E.fail_rows = d_fail_rows;
+    P->last_launches = 0;
+    reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
+    P->last_launches++;
+    int nblocks = 0;
+    if (i1 > i0) {
+        const int layout = resolve_layout(P, family, q);
+        if (P->timing)
+            CUDA_TRY(cudaEventRecord(P->ev0, P->stream));
+        if (layout == VB200_LAYOUT_TILED_REG) {
+            if (!tiled_supported(family, P->mp1, P->p, P->d, q))
+                return fail(VB200_EUNSUPPORTED, "TILED_REG layout does not support this shape");
+            rc = launch_tiled(P->stream, P->sm_count, P->smem_optin, E, &nblocks, &P->last_kernel,
+                              [&](size_t doubles) -> double * {
+                                  return ensure_partials(P, doubles) == VB200_OK ? P->partials : nullptr;
+                              });
+            if (rc == -100)
+                return fail(VB200_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(cudaGetLastError()));
+            if (rc)
+                return fail(rc, "tiled launch failed");
+        } else if (layout == VB200_LAYOUT_WARP_SMEM) {
+            rc = launch_warp_smem(P, E, &nblocks);
+            if (rc)
+                return rc;
+        } else {
+            return fail(VB200_EUNSUPPORTED, "THREAD_SMEM layout is not built in this version");
+        }
+        P->last_launches++;
+        if (P->timing)
+            CUDA_TRY(cudaEventRecord(P->ev1, P->stream));
+    } else {
+        P->last_kernel = "";
+    }
+    rc = ensure_partials(P, 1);
+    if (rc)
+        return rc;
+    reduce_partials_kernel<<<1, 256, 256 * sizeof(double), P->stream>>>(P->partials, nblocks, E.L, d_out,
+                                                                        P->fail_word, P->fail_count);
+    CUDA_TRY(cudaGetLastError());
+    P->last_launches++;
+    return VB200_OK;
+}
+
+extern "C" int vb200_eval_async(vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
+                                int64_t i1, double *d_out)
+{
+    if (!d_out)
+        return fail(VB200_EINVAL, "d_out is NULL");
+    return enqueue_eval(P, family, theta, q, jitter, i0, i1, d_out, nullptr, nullptr);
+}
+
+extern "C" int vb200_sync(vb200_problem *P)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    CUDA_TRY(cudaSetDevice(P->device));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return VB200_OK;
+}
+
+extern "C" int vb200_fail_info(vb200_problem *P, int64_t *first_fail, int32_t *pivot)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    CUDA_TRY(cudaSetDevice(P->device));
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    const unsigned long long w = *P->h_fail;
+    if (w == ~0ull) {
+        if (first_fail) *first_fail = -1;
+        if (pivot) *pivot = -1;
+    } else {
+        if (first_fail) *first_fail = (int64_t)(w >> 16);
+        if (pivot) *pivot = (int32_t)(w & 0xffff) - 1;
+    }
+    return VB200_OK;
+}
+
+extern "C" int vb200_eval(vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
+                          int64_t i1, double *out_sums, int64_t *first_fail, int32_t *pivot)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    if (!out_sums)
+        return fail(VB200_EINVAL, "out_sums is NULL");
+    CUDA_TRY(cudaSetDevice(P->device));
+    const int want = vb200_family_nparms(family, P->d);
+    if (want < 0 || q != want)
+        return fail(VB200_EINVAL, "theta has the wrong length for this family and d");
+    const size_t L = (size_t)vb200_acc_len(P->p, q);
+    if (P->d_out_cap < L + 2) {
+        if (P->d_out) cudaFree(P->d_out);
+        P->d_out = nullptr;
+        P->d_out_cap = 0;
+        CUDA_TRY(cudaMalloc(&P->d_out, sizeof(double) * (L + 2)));
+        P->d_out_cap = L + 2;
+    }
+    if (P->h_out_cap < L + 2) {
+        if (P->h_out) cudaFreeHost(P->h_out);
+        P->h_out = nullptr;
+        P->h_out_cap = 0;
+        CUDA_TRY(cudaMallocHost(&P->h_out, sizeof(double) * (L + 2)));
+        P->h_out_cap = L + 2;
+    }
+    int rc = enqueue_eval(P, family, theta, q, jitter, i0, i1, P->d_out, nullptr, nullptr);
+    if (rc)
+        return rc;
+    CUDA_TRY(cudaMemcpyAsync(P->h_out, P->d_out, sizeof(double) * (L + 2), cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    memcpy(out_sums, P->h_out, sizeof(double) * L);
+    const unsigned long long w = *P->h_fail;
+    if (P->h_out[L] > 0.0 && w != ~0ull) {
+        if (first_fail) *first_fail = (int64_t)(w >> 16);
+        if (pivot) *pivot = (int32_t)(w & 0xffff) - 1;
+    } else {
+        if (first_fail) *first_fail = -1;
+        if (pivot) *pivot = -1;
+    }
+    return VB200_OK;
+}
+
+extern "C" int vb200_eval_rows(vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
+                               int64_t i1, double *rows_host, int32_t *fail_host)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    if (!rows_host || !fail_host)
+        return fail(VB200_EINVAL, "NULL output");
+    CUDA_TRY(cudaSetDevice(P->device));
+    const int want = vb200_family_nparms(family, P->d);
+    if (want < 0 || q != want)
+        return fail(VB200_EINVAL, "theta has the wrong length for this family and d");
+    const size_t L = (size_t)vb200_acc_len(P->p, q);
+    const size_t cnt = (size_t)(i1 > i0 ? i1 - i0 : 0);
+    if (cnt == 0)
+        return VB200_OK;
+    double *d_rows = nullptr, *d_tot = nullptr;
+    int *d_fail = nullptr;
+    CUDA_TRY(cudaMalloc(&d_rows, sizeof(double) * cnt * L));
+    CUDA_TRY(cudaMalloc(&d_fail, sizeof(int) * cnt));
+    CUDA_TRY(cudaMalloc(&d_tot, sizeof(double) * (L + 2)));
+    cudaMemsetAsync(d_rows, 0, sizeof(double) * cnt * L, P->stream);
+    cudaMemsetAsync(d_fail, 0, sizeof(int) * cnt, P->stream);
+    int rc = enqueue_eval(P, family, theta, q, jitter, i0, i1, d_tot, d_rows, d_fail);
+    if (rc == VB200_OK) {
+        cudaError_t e1 = cudaMemcpyAsync(rows_host, d_rows, sizeof(double) * cnt * L, cudaMemcpyDeviceToHost, P->stream);
+        cudaError_t e2 = cudaMemcpyAsync(fail_host, d_fail, sizeof(int) * cnt, cudaMemcpyDeviceToHost, P->stream);
+        cudaError_t e3 = cudaStreamSynchronize(P->stream);
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+            rc = fail(VB200_ECUDA, std::string("eval_rows copy: ") +
+                                       cudaGetErrorString(e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3)));
+    }
+    cudaFree(d_rows);
+    cudaFree(d_fail);
+    cudaFree(d_tot);
+    return rc;
+}
+
+extern "C" int vb200_enable_timing(vb200_problem *P, int on)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    CUDA_TRY(cudaSetDevice(P->device));
+    if (on && !P->ev0) {
+        CUDA_TRY(cudaEventCreate(&P->ev0));
+        CUDA_TRY(cudaEventCreate(&P->ev1));
+    }
+    P->timing = on != 0;
+    return VB200_OK;
+}
+
+extern "C" int vb200_last_kernel_ms(vb200_problem *P, double *ms)
+{
+    if (!P || !ms)
+        return fail(VB200_EINVAL, "NULL argument");
+    if (!P->timing || !P->ev0)
+        return fail(VB200_EINVAL, "timing is not enabled");
+    CUDA_TRY(cudaSetDevice(P->device));
+    CUDA_TRY(cudaEventSynchronize(P->ev1));
+    float f = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&f, P->ev0, P->ev1));
+    *ms = (double)f;
+    return VB200_OK;
+}
+
+extern "C" int vb200_last_launch_count(const vb200_problem *P) { return P ? P->last_launches : 0; }
+extern "C" const char *vb200_last_kernel_name(const vb200_problem *P) { return P ? P->last_kernel : ""; }
+
+extern "C" int vb200_measure_fp64_peak(int device, double seconds, double *tflops, double *sustained)
+{
+    if (!tflops || !sustained)
+        return fail(VB200_EINVAL, "output pointer is NULL");
+    if (vb200_device_count() <= device || device < 0)
+        return fail(VB200_ECUDA, "no such CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    double *sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    const int threads = 256, blocks = prop.multiProcessorCount * 4, iters = 4096;
+    const double flops_per_launch = 2.0 * 16.0 * 8.0 * (double)iters * threads * (double)blocks;
+    double best = 0.0, elapsed = 0.0, total_flops = 0.0;
+    dfma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-9); // warm-up
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (seconds <= 0.0)
+        seconds = 0.2;
+    while (elapsed < seconds) {
+        CUDA_TRY(cudaEventRecord(e0));
+        dfma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-9);
+        CUDA_TRY(cudaEventRecord(e1));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        elapsed += ms * 1e-3;
+        total_flops += flops_per_launch;
+        const double tf = flops_per_launch / (ms * 1e-3) * 1e-12;
+        if (tf > best)
+            best = tf;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    *tflops = best;
+    *sustained = total_flops / elapsed * 1e-12;
+    return VB200_OK;
+}

@@ -1,0 +1,320 @@
+"""Engine facade: ``run`` sums the per-observation Vecchia contributions on the GPU.
+
+Keeps the reference facade's call signature and result type
+(/root/reference/pkg/src/vecchiagp/engine/__init__.py: ``run`` :196-248, ``VecchiaParts``
+:103-121, ``available_cores`` / ``active_core_name`` :64-73, ``choose_capacity_tier``
+:76-85) and plugs in ONE core, ``"cuda"``: the sm_100a kernels behind the C ABI of
+include/vecchia_b200.h.  What the reference does per call on the host -- slot
+allocation, head pass, tail pass, host reduction (:233-248) -- happens inside a single
+fused kernel launch plus a fixed-order device reduction; only the L totals and a
+failure word come back.
+
+``backend``, ``workers`` and ``capacity_tier`` are accepted for signature
+compatibility (and validated like the reference does) but do not select different
+code: there is one CUDA schedule.  ``deterministic`` is always honoured -- the device
+reduction order is fixed, so results are run-to-run reproducible for a given GPU.
+
+The reference's "compiled" and "fallback" CPU cores are NOT part of this package
+and there is no CPU fallback: without the built library and a CUDA device, ``run``
+raises ``DeviceUnavailable``.
+"""
+from __future__ import annotations
+
+import ctypes
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from .. import _cabi
+from ..covariance import covariance_registry, validate_parameters
+from ..errors import DeviceUnavailable, NotPositiveDefinite
+from ..model import CovarianceParameters, Dataset, normalize_backend
+from ..preprocess import NeighborArray
+
+CAPACITY_TIERS = (8, 16, 32, 64)
+VB_MAX_Q = 22  # csrc/common.cuh VB_MAXQ
+CORES = ("cuda",)
+_REFERENCE_CORES = ("compiled", "fallback")
+
+
+def available_cores() -> tuple:
+    return CORES
+
+
+def active_core_name() -> str:
+    return "cuda"
+
+
+def choose_capacity_tier(mp1: int) -> int:
+    """Smallest tier holding a conditioning set of m+1 points (exact size above 64)."""
+    for tier in CAPACITY_TIERS:
+        if mp1 <= tier:
+            return tier
+    return mp1
+
+
+@dataclass(frozen=True)
+class VecchiaParts:
+    """Totals over all observations: ``logdet``/``ysy`` build the log-likelihood, ``xsx``/``ysx``
+    profile the mean, the d-fields are their parameter derivatives, ``ainfo`` is the Fisher
+    information of the covariance parameters."""
+
+    logdet: float
+    ysy: float
+    xsx: np.ndarray
+    ysx: np.ndarray
+    dlogdet: np.ndarray
+    dysy: np.ndarray
+    dysx: np.ndarray
+    dxsx: np.ndarray
+    ainfo: np.ndarray
+
+
+def acc_len(p: int, q: int) -> int:
+    return (1 + q) * (2 + p + p * p) + q * q
+
+
+def parts_from_flat(v, p: int, q: int) -> VecchiaParts:
+    """Split the flat accumulator vector (C order of the reference's slot arrays,
+    engine/__init__.py:141-152) into ``VecchiaParts``."""
+    v = np.asarray(v, dtype=np.float64)
+    cuts = np.cumsum([1, 1, p * p, p, q, q, p * q, p * p * q, q * q])
+    logdet, ysy, xsx, ysx, dlogdet, dysy, dysx, dxsx, ainfo = np.split(v[:cuts[-1]], cuts[:-1])
+    return VecchiaParts(float(logdet[0]), float(ysy[0]), xsx.reshape(p, p).copy(), ysx.copy(), dlogdet.copy(),
+                        dysy.copy(), dysx.reshape(p, q).copy(), dxsx.reshape(p, p, q).copy(),
+                        ainfo.reshape(q, q).copy())
+
+
+def flat_from_parts(parts: VecchiaParts) -> np.ndarray:
+    return np.concatenate([np.atleast_1d(np.asarray(x, dtype=np.float64)).ravel() for x in (
+        parts.logdet, parts.ysy, parts.xsx, parts.ysx, parts.dlogdet, parts.dysy, parts.dysx, parts.dxsx,
+        parts.ainfo)])
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as err:  # pragma: no cover
+        raise DeviceUnavailable("PyTorch is required for device buffers") from err
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device is visible; the cuda core has no CPU fallback")
+    return torch
+
+
+class DeviceProblem:
+    """Device-resident inputs of one dataset (or one contiguous shard of its rows).
+
+    PyTorch owns the device buffers (``y``, ``X``, working ``locs``, ``nn`` rows
+    ``[row0, row0+rows)``); the C library adopts their pointers and packs its own
+    point records.  Upload happens once here -- a Fisher-scoring fit then only
+    sends theta down and gets L doubles back per evaluation.
+    """
+
+    def __init__(self, ds: Dataset, nn: NeighborArray, family: str, device=None, row0: int = 0,
+                 rows: int | None = None, layout: str = "auto", nn_is_shard: bool = False):
+        """``nn`` is the full (n, m+1) table, or -- with ``nn_is_shard`` -- only its rows
+        [row0, row0+rows) (what each rank of a sharded run builds for itself)."""
+        torch = _torch()
+        lib = _cabi.load()
+        fam = covariance_registry(family)
+        n, p = ds.n, ds.p
+        rows = (nn.idx.shape[0] if nn_is_shard else n - row0) if rows is None else rows
+        if row0 < 0 or rows < 0 or row0 + rows > n:
+            raise ValueError("shard rows outside [0, n)")
+        if nn.idx.shape[0] != (rows if nn_is_shard else n):
+            raise ValueError(f"neighbor table has {nn.idx.shape[0]} rows for n={n}")
+        shard_rows = nn.idx if nn_is_shard else nn.idx[row0:row0 + rows]
+        work = fam.prepare_locs(ds.locs)
+        self.family_name, self.kernel_code = family, fam.kernel_code
+        self.n, self.p, self.d, self.mp1 = n, p, work.shape[1], nn.idx.shape[1]
+        self.row0, self.rows = row0, rows
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream()
+            put = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=True)
+            self._y, self._X, self._locs = put(ds.y), put(ds.X), put(work)
+            self._nn = put(shard_rows) if rows > 0 else torch.zeros((1, self.mp1), dtype=torch.int64,
+                                                                                  device=self.device)
+            self._out = torch.zeros(acc_len(p, VB_MAX_Q) + 2, dtype=torch.float64, device=self.device)
+            handle = ctypes.c_void_p()
+            rc = lib.vb200_create(self.device.index or 0, n, p, self.d, self.mp1, self._y.data_ptr(),
+                                  self._X.data_ptr(), self._locs.data_ptr(), self._nn.data_ptr(), row0, rows,
+                                  ctypes.c_void_p(stream.cuda_stream), ctypes.byref(handle))
+            _cabi.check(rc, "vb200_create")
+        self._h = handle
+        self._lib = lib
+        if layout != "auto":
+            self.set_layout(layout)
+
+    # -- lifetime ---------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h:
+            self._lib.vb200_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- configuration ----------------------------------------------------------
+    def set_layout(self, layout: str):
+        _cabi.check(self._lib.vb200_set_layout(self._h, _cabi.LAYOUTS[layout]), "vb200_set_layout")
+
+    def layout_for(self, q: int) -> str:
+        return _cabi.LAYOUT_NAMES[self._lib.vb200_get_layout(self._h, self.kernel_code, q)]
+
+    def use_current_stream(self):
+        torch = _torch()
+        with torch.cuda.device(self.device):
+            s = torch.cuda.current_stream().cuda_stream
+        _cabi.check(self._lib.vb200_set_stream(self._h, ctypes.c_void_p(s)), "vb200_set_stream")
+
+    def enable_timing(self, on: bool = True):
+        _cabi.check(self._lib.vb200_enable_timing(self._h, int(on)), "vb200_enable_timing")
+
+    def last_kernel_ms(self) -> float:
+        ms = ctypes.c_double(0.0)
+        _cabi.check(self._lib.vb200_last_kernel_ms(self._h, ctypes.byref(ms)), "vb200_last_kernel_ms")
+        return ms.value
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self._lib.vb200_last_launch_count(self._h))
+
+    @property
+    def last_kernel_name(self) -> str:
+        return (self._lib.vb200_last_kernel_name(self._h) or b"").decode()
+
+    # -- evaluation ---------------------------------------------------------------
+    def _theta(self, theta):
+        th = np.ascontiguousarray(theta, dtype=np.float64).ravel()
+        return th, th.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+    def totals(self, theta, jitter: float = 0.0, i0: int | None = None, i1: int | None = None) -> np.ndarray:
+        """Flat totals (L,) over [i0, i1) of this shard; raises NotPositiveDefinite."""
+        th, thp = self._theta(theta)
+        q = th.shape[0]
+        i0 = self.row0 if i0 is None else i0
+        i1 = self.row0 + self.rows if i1 is None else i1
+        out = np.empty(acc_len(self.p, q))
+        first, piv = ctypes.c_int64(-1), ctypes.c_int32(-1)
+        rc = self._lib.vb200_eval(self._h, self.kernel_code, thp, q, float(jitter), int(i0), int(i1),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(first),
+                                  ctypes.byref(piv))
+        _cabi.check(rc, "vb200_eval")
+        if first.value >= 0:
+            raise NotPositiveDefinite(pivot=piv.value, observation=first.value)
+        return out
+
+    def totals_async(self, theta, jitter: float = 0.0, i0: int | None = None, i1: int | None = None):
+        """Enqueue one evaluation; returns the device tensor (L+2,) described in
+        include/vecchia_b200.h (totals, failure count, -(first failing index)-1)."""
+        th, thp = self._theta(theta)
+        q = th.shape[0]
+        i0 = self.row0 if i0 is None else i0
+        i1 = self.row0 + self.rows if i1 is None else i1
+        L = acc_len(self.p, q)
+        rc = self._lib.vb200_eval_async(self._h, self.kernel_code, thp, q, float(jitter), int(i0), int(i1),
+                                        ctypes.c_void_p(self._out.data_ptr()))
+        _cabi.check(rc, "vb200_eval_async")
+        return self._out[:L + 2]
+
+    def fail_info(self):
+        first, piv = ctypes.c_int64(-1), ctypes.c_int32(-1)
+        _cabi.check(self._lib.vb200_fail_info(self._h, ctypes.byref(first), ctypes.byref(piv)), "vb200_fail_info")
+        return first.value, piv.value
+
+    def rows_host(self, theta, jitter: float = 0.0, i0: int | None = None, i1: int | None = None):
+        """Per-observation accumulator rows (i1-i0, L) and pivot+1 failure flags (diagnostics)."""
+        th, thp = self._theta(theta)
+        q = th.shape[0]
+        i0 = self.row0 if i0 is None else i0
+        i1 = self.row0 + self.rows if i1 is None else i1
+        rows = np.zeros((max(i1 - i0, 0), acc_len(self.p, q)))
+        flags = np.zeros(max(i1 - i0, 0), dtype=np.int32)
+        rc = self._lib.vb200_eval_rows(self._h, self.kernel_code, thp, q, float(jitter), int(i0), int(i1),
+                                       rows.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+        _cabi.check(rc, "vb200_eval_rows")
+        return rows, flags
+
+    def run(self, cov: CovarianceParameters, jitter: float = 0.0) -> VecchiaParts:
+        if cov.family != self.family_name:
+            raise ValueError(f"problem was built for {self.family_name!r}, got {cov.family!r}")
+        return parts_from_flat(self.totals(cov.theta, jitter), self.p, cov.nparms)
+
+
+# ---------------------------------------------------------------------------
+# facade with a small device-problem cache (upload once per dataset, not per call)
+# ---------------------------------------------------------------------------
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_SLOTS = 2
+
+
+def clear_cache() -> None:
+    while _CACHE:
+        _, (prob, _keep) = _CACHE.popitem()
+        prob.close()
+
+
+def _cached_problem(ds: Dataset, nn: NeighborArray, family: str) -> DeviceProblem:
+    prep = "sphere" if family == "exponential_sphere" else "raw"
+    key = (ds.y.ctypes.data, ds.X.ctypes.data, ds.locs.ctypes.data, nn.idx.ctypes.data, ds.n, ds.p, ds.d,
+           nn.idx.shape[1], prep, covariance_registry(family).kernel_code)
+    hit = _CACHE.get(key)
+    if hit is not None:
+        _CACHE.move_to_end(key)
+        return hit[0]
+    prob = DeviceProblem(ds, nn, family)
+    # keep the host arrays alive so their addresses cannot be recycled while cached
+    _CACHE[key] = (prob, (ds.y, ds.X, ds.locs, nn.idx))
+    while len(_CACHE) > _CACHE_SLOTS:
+        _, (old, _keep) = _CACHE.popitem(last=False)
+        old.close()
+    return prob
+
+
+def run(ds: Dataset, nn: NeighborArray, cov: CovarianceParameters, backend: str = "task",
+        deterministic: bool = True, workers: int | None = None, capacity_tier: int | None = None,
+        jitter: float = 0.0, core: str | None = None) -> VecchiaParts:
+    """Sum of every observation's contribution (drop-in for the reference's ``engine.run``).
+
+    Raises ``NotPositiveDefinite`` with the lowest failing observation index when a local
+    factorization fails; no jitter is added unless requested.
+    """
+    normalize_backend(backend)
+    core = core or "cuda"
+    if core in _REFERENCE_CORES:
+        raise ValueError(f"core {core!r} is a CPU core of the reference package; this package provides 'cuda' only")
+    if core != "cuda":
+        raise ValueError(f"unknown core {core!r}")
+    validate_parameters(cov, ds.d)
+    mp1 = nn.idx.shape[1]
+    if nn.idx.shape[0] != ds.n:
+        raise ValueError(f"neighbor table has {nn.idx.shape[0]} rows for n={ds.n}")
+    if capacity_tier is not None and capacity_tier < mp1:
+        raise ValueError(f"capacity tier {capacity_tier} too small for m+1={mp1}")
+    prob = _cached_problem(ds, nn, cov.family)
+    return prob.run(cov, jitter=float(jitter))
+
+
+def process_observation(i: int, ds: Dataset, nn: NeighborArray, cov: CovarianceParameters,
+                        jitter: float = 0.0) -> VecchiaParts:
+    """One observation's contribution (reference: engine/__init__.py:179-193), from the GPU."""
+    if not 0 <= i < ds.n:
+        raise IndexError(f"observation index {i} outside [0, {ds.n})")
+    validate_parameters(cov, ds.d)
+    prob = _cached_problem(ds, nn, cov.family)
+    rows, flags = prob.rows_host(cov.theta, jitter, i, i + 1)
+    if flags[0]:
+        raise NotPositiveDefinite(pivot=int(flags[0]) - 1, observation=i)
+    return parts_from_flat(rows[0], ds.p, cov.nparms)

@@ -1,0 +1,278 @@
+"""GPU parity tests: the CUDA core (through the C ABI) against the CPU oracle and the
+reference's golden fixtures.  Tolerances are BASELINE.json's: loglik 1e-9 relative,
+gradient / Fisher information 1e-7 relative, fitted parameters 1e-6 relative.
+Patterns follow the reference's own tests (pkg/tests/test_engine.py, test_inference.py,
+test_acceptance.py)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2407_02740_b200 as vg
+from paper_2407_02740_b200 import engine
+from paper_2407_02740_b200.engine import DeviceProblem, flat_from_parts
+
+from oracle import vecchia_oracle as vo
+from conftest import make_instance
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = ["warp_smem", "tiled_reg"]
+
+CASES = ["iso_d2_p2_m9", "iso_d2_p1_m30", "iso_d3_p4_m30", "aniso_d3_p2_m8", "aniso_d2_p1_m20",
+         "sphere_p1_m12", "iso_jitter", "iso_heads_only", "iso_wide_m79", "iso_zero_nugget",
+         "iso_d1_m5", "iso_m60"]
+
+
+def fields_close(got, want, p, q, rtol):
+    """Field-by-field comparison, relative to each field's largest magnitude (entries of a
+    field that cancel to ~0 are compared on the field's scale, as the reference's
+    parts_close does with its atol; pkg/tests/conftest.py:41-64)."""
+    G, W = vo.split_acc(np.asarray(got), p, q), vo.split_acc(np.asarray(want), p, q)
+    for name in W:
+        w, g = np.asarray(W[name], dtype=np.float64), np.asarray(G[name], dtype=np.float64)
+        scale = max(float(np.max(np.abs(w))), 1e-300)
+        err = float(np.max(np.abs(g - w))) / scale
+        assert err <= rtol, f"{name}: relative error {err:.3e} > {rtol:.1e}"
+
+
+def layouts_for(prob, q):
+    """Layouts to exercise for this shape: always warp_smem, plus tiled_reg when supported."""
+    out = ["warp_smem"]
+    prob.set_layout("auto")
+    if prob.layout_for(q) == "tiled_reg":
+        out.append("tiled_reg")
+    return out
+
+
+def _golden(z, name):
+    g = lambda k: z[f"{name}/{k}"]
+    return dict(y=g("y"), X=g("X"), locs=g("locs"), nn=g("nn"), theta=g("theta"), family=str(g("family")),
+                jitter=float(g("jitter")), totals=g("totals_compiled"), loglik=float(g("loglik_compiled")),
+                grad=g("grad_compiled"))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_totals_match_reference(engine_cases, name):
+    c = _golden(engine_cases, name)
+    ds = vg.Dataset(c["y"], c["X"], c["locs"])
+    nn = vg.NeighborArray(c["nn"])
+    p, q = ds.p, c["theta"].shape[0]
+    with DeviceProblem(ds, nn, c["family"]) as prob:
+        for layout in layouts_for(prob, q):
+            prob.set_layout(layout)
+            tot = prob.totals(c["theta"], jitter=c["jitter"])
+            fields_close(tot, c["totals"], p, q, 1e-9)
+            ev = vg.assemble(engine.parts_from_flat(tot, p, q), ds.n)
+            assert ev.loglik == pytest.approx(c["loglik"], rel=1e-9)
+            gscale = np.max(np.abs(c["grad"]))
+            assert np.max(np.abs(ev.grad - c["grad"])) <= 1e-7 * gscale
+
+
+@pytest.mark.parametrize("name", ["iso_d2_p2_m9", "aniso_d3_p2_m8", "iso_heads_only", "iso_d3_p4_m30"])
+def test_per_observation_rows_match_oracle(engine_cases, name):
+    c = _golden(engine_cases, name)
+    ds = vg.Dataset(c["y"], c["X"], c["locs"])
+    nn = vg.NeighborArray(c["nn"])
+    fam = vg.covariance_registry(c["family"])
+    work = fam.prepare_locs(ds.locs)
+    want, _ = vo.observations(ds.y, ds.X, work, nn.idx, c["family"], c["theta"], jitter=c["jitter"])
+    with DeviceProblem(ds, nn, c["family"]) as prob:
+        for layout in layouts_for(prob, c["theta"].shape[0]):
+            prob.set_layout(layout)
+            rows, flags = prob.rows_host(c["theta"], c["jitter"])
+            assert not flags.any()
+            np.testing.assert_allclose(rows, want, rtol=1e-8, atol=1e-9)
+
+
+def test_engine_run_facade_and_process_observation(engine_cases):
+    c = _golden(engine_cases, "iso_d2_p2_m9")
+    ds = vg.Dataset(c["y"], c["X"], c["locs"])
+    nn = vg.NeighborArray(c["nn"])
+    cov = vg.CovarianceParameters(c["family"], c["theta"])
+    parts = engine.run(ds, nn, cov, backend="task", deterministic=True, workers=3, core="cuda")
+    fields_close(flat_from_parts(parts), c["totals"], ds.p, cov.nparms, 1e-9)
+    again = engine.run(ds, nn, cov)  # cached device problem, bit-reproducible
+    assert np.array_equal(flat_from_parts(parts), flat_from_parts(again))
+    one = engine.process_observation(17, ds, nn, cov)
+    want, _ = vo.observations(ds.y, ds.X, ds.locs, nn.idx, c["family"], c["theta"], i0=17, i1=18)
+    np.testing.assert_allclose(flat_from_parts(one), want[0], rtol=1e-8, atol=1e-10)
+    with pytest.raises(ValueError):
+        engine.run(ds, nn, cov, core="compiled")
+    with pytest.raises(ValueError):
+        engine.run(ds, nn, cov, backend="gpu")
+    with pytest.raises(ValueError):
+        engine.run(ds, nn, cov, capacity_tier=4)
+    with pytest.raises(ValueError):
+        engine.run(ds, nn, vg.CovarianceParameters(c["family"], [1.0, -0.2, 0.1]))
+    engine.clear_cache()
+
+
+def test_k1_closed_form_and_zero_response():
+    # reference tests/test_engine.py:93-114
+    sig2, rho, tau2 = 1.7, 0.3, 0.2
+    ds = vg.Dataset([0.8], [[1.0]], [[0.1, 0.2]])
+    nn = vg.NeighborArray(np.array([[0]]))
+    parts = engine.run(ds, nn, vg.CovarianceParameters("exponential_isotropic", [sig2, rho, tau2]))
+    v = sig2 * (1 + tau2)
+    assert parts.logdet == pytest.approx(np.log(v), rel=1e-13)
+    assert parts.ysy == pytest.approx(0.64 / v, rel=1e-13)
+    assert parts.xsx[0, 0] == pytest.approx(1 / v, rel=1e-13)
+    y, X, locs, theta = make_instance(3, 50, 2, 2)
+    nn = vg.find_ordered_neighbors(locs, 6)
+    zero = engine.run(vg.Dataset(np.zeros(50), X, locs), nn, vg.CovarianceParameters("exponential_isotropic", theta))
+    assert zero.ysy == 0.0 and not zero.ysx.any() and not zero.dysy.any() and not zero.dysx.any()
+    engine.clear_cache()
+
+
+def test_not_positive_definite_reports_observation_and_pivot(failure_case):
+    # reference tests/test_engine.py:230-253: duplicated location, zero nugget -> observation 7
+    z = failure_case
+    n = z["y"].shape[0]
+    ds = vg.Dataset(z["y"], np.ones((n, 1)), z["locs"])
+    nn = vg.NeighborArray(z["nn"])
+    cov = vg.CovarianceParameters("exponential_isotropic", z["theta"])
+    with DeviceProblem(ds, nn, cov.family) as prob:
+        for layout in layouts_for(prob, 3):
+            prob.set_layout(layout)
+            with pytest.raises(vg.NotPositiveDefinite) as err:
+                prob.run(cov)
+            assert err.value.observation == int(z["observation_compiled"]) == 7
+            assert err.value.pivot == int(z["pivot_compiled"])
+            rescued = prob.totals(cov.theta, jitter=1e-6)
+            fields_close(rescued, z["rescued_totals"], 1, 3, 1e-6)  # near-singular K: conditioning-limited
+
+
+FAMILY_SHAPES = [
+    ("exponential_isotropic", 2, 1, [1.5, 0.25, 0.1], 30),
+    ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 30),
+    ("matern25_isotropic", 2, 2, [1.2, 0.06, 0.05], 20),
+    ("matern15_isotropic", 3, 4, [1.0, 0.15, 0.1], 30),
+    ("exponential_spacetime", 3, 1, [1.3, 0.2, 0.5, 0.1], 30),
+    ("exponential_anisotropic", 3, 1, [1.3, 0.2, 0.3, 0.5, 0.1], 10),
+    ("exponential_isotropic", 2, 1, [1.5, 0.25, 0.1], 10),
+    ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 40),
+    ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 60),
+    ("exponential_isotropic", 2, 3, [1.5, 0.25, 0.1], 15),
+]
+
+
+@pytest.mark.parametrize("family,d,p,theta,m", FAMILY_SHAPES)
+def test_families_and_shapes_against_oracle(family, d, p, theta, m):
+    n = 3000
+    y, X, locs, theta = make_instance(100 + m + d, n, d, p, family, theta)
+    nn = vg.find_ordered_neighbors(locs, m)
+    want = vo.run(y, X, locs, nn.idx, family, theta, deterministic=True)
+    q = theta.shape[0]
+    ev_want = vo.assemble(want, n, p, q)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, family) as prob:
+        for layout in layouts_for(prob, q):
+            prob.set_layout(layout)
+            got = prob.totals(theta)
+            fields_close(got, want, p, q, 1e-9)
+            ev = vg.assemble(engine.parts_from_flat(got, p, q), n)
+            assert ev.loglik == pytest.approx(ev_want["loglik"], rel=1e-9)
+            assert np.max(np.abs(ev.grad - ev_want["grad"])) <= 1e-7 * np.max(np.abs(ev_want["grad"]))
+            assert np.max(np.abs(ev.info - ev_want["info"])) <= 1e-7 * np.max(np.abs(ev_want["info"]))
+            again = prob.totals(theta)
+            assert np.array_equal(got, again), "device reduction must be run-to-run reproducible"
+
+
+def test_shard_sums_equal_whole_and_empty_range():
+    y, X, locs, theta = make_instance(9, 5000, 2, 1)
+    nn = vg.find_ordered_neighbors(locs, 30)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "exponential_isotropic") as prob:
+        whole = prob.totals(theta)
+        cuts = [0, 7, 31, 1250, 1251, 4000, 5000]
+        parts = sum(prob.totals(theta, i0=a, i1=b) for a, b in zip(cuts[:-1], cuts[1:]))
+        fields_close(parts, whole, 1, 3, 1e-11)
+        assert not prob.totals(theta, i0=100, i1=100).any()
+    # a problem holding only a shard of the neighbor rows (the multi-GPU layout)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "exponential_isotropic", row0=1250, rows=2750) as shard:
+        got = shard.totals(theta)
+        want = vo.run(y, X, locs, nn.idx, "exponential_isotropic", theta, i0=1250, i1=4000)
+        fields_close(got, want, 1, 3, 1e-9)
+        with pytest.raises(ValueError):
+            shard.totals(theta, i0=0, i1=10)
+
+
+def test_within_row_order_invariance():
+    # reference tests/test_engine.py:169-185: permuting the neighbors of a row changes nothing
+    y, X, locs, theta = make_instance(4, 400, 2, 1)
+    nn = vg.find_ordered_neighbors(locs, 12).idx.copy()
+    rng = np.random.default_rng(0)
+    shuffled = nn.copy()
+    for i in range(13, 400):
+        shuffled[i, 1:] = rng.permutation(shuffled[i, 1:])
+    ds = vg.Dataset(y, X, locs)
+    a = flat_from_parts(engine.run(ds, vg.NeighborArray(nn), vg.CovarianceParameters("exponential_isotropic", theta)))
+    b = flat_from_parts(engine.run(ds, vg.NeighborArray(shuffled),
+                                   vg.CovarianceParameters("exponential_isotropic", theta)))
+    fields_close(b, a, 1, 3, 1e-10)
+    engine.clear_cache()
+
+
+@pytest.mark.parametrize("tag", ["cli300_a", "cli300_b", "aniso400"])
+def test_full_fit_matches_reference(fit_cases, tag):
+    z = fit_cases
+    g = lambda k: z[f"{tag}/{k}"]
+    ds = vg.Dataset(g("y"), g("X"), g("locs"))
+    nn = vg.NeighborArray(g("nn"))
+    family = str(g("family"))
+    start = vg.CovarianceParameters(family, g("start"))
+    np.testing.assert_allclose(vg.default_start(ds, family).theta, start.theta, rtol=1e-12)
+    res = vg.fit(ds, nn, vg.ModelSpec(covariance=start, m=int(g("m"))))
+    np.testing.assert_allclose(res.theta_hat.theta, g("compiled/theta_hat"), rtol=1e-6)
+    np.testing.assert_allclose(res.beta_hat, g("compiled/beta_hat"), rtol=1e-6, atol=1e-9)
+    assert res.loglik == pytest.approx(float(g("compiled/trace")[-1]), rel=1e-9)
+    assert res.converged == bool(g("compiled/converged"))
+    assert all(b >= a for a, b in zip(res.loglik_trace, res.loglik_trace[1:]))
+    engine.clear_cache()
+
+
+def test_config1_fit_n10000_m30(config1_golden):
+    """BASELINE.json configs[0]: n=10 000 2-D, exponential_isotropic, m=30, full fit."""
+    z = config1_golden
+    n, m, seed = 10_000, int(z["m"]), int(z["seed"])
+    rng = np.random.default_rng(seed)
+    locs = rng.uniform(0.0, 1.0, (n, 2))
+    locs = locs[vg.random_permutation(n, seed).perm]
+    nn = vg.find_ordered_neighbors(locs, m, method="grid")
+    assert int(nn.idx.sum()) == int(z["nn_checksum"]) and np.array_equal(nn.idx[9999], z["nn_row_9999"])
+    ds = vg.Dataset(z["y"], np.ones((n, 1)), locs)
+    start = vg.default_start(ds, "exponential_isotropic")
+    np.testing.assert_allclose(start.theta, z["start"], rtol=1e-12)
+    ev0 = vg.evaluate(ds, nn, start)
+    assert ev0.loglik == pytest.approx(float(z["loglik_start"]), rel=1e-9)
+    np.testing.assert_allclose(ev0.grad, z["grad_start"], rtol=1e-7)
+    np.testing.assert_allclose(ev0.info, z["info_start"], rtol=1e-7)
+    res = vg.fit(ds, nn, vg.ModelSpec(covariance=start, m=m))
+    np.testing.assert_allclose(res.theta_hat.theta, z["fit/theta_hat"], rtol=1e-6)
+    np.testing.assert_allclose(res.beta_hat, z["fit/beta_hat"], rtol=1e-6)
+    assert res.loglik == pytest.approx(float(z["fit/trace"][-1]), rel=1e-9)
+    np.testing.assert_allclose(res.fisher_info, z["fit/fisher_info"], rtol=1e-5)
+    engine.clear_cache()
+
+
+def test_full_size_properties_n2_20():
+    """BASELINE.json configs[1] shape (n = 2^20, m = 30, Matern 3/2): size-independent
+    properties -- shard additivity, run-to-run reproducibility, oracle agreement on a
+    prefix, and the analytic identities dlogdet_0 = n / sigma^2, ainfo_00 = n / (2 sigma^4)."""
+    n, m = 1 << 20, 30
+    rng = np.random.default_rng(2407)
+    locs = rng.uniform(0.0, 1.0, (n, 2))
+    y = rng.normal(size=n)
+    X = np.ones((n, 1))
+    theta = np.array([1.0, 0.002, 0.1])
+    nn = vg.find_ordered_neighbors(locs, m)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern15_isotropic") as prob:
+        whole = prob.totals(theta)
+        assert np.array_equal(whole, prob.totals(theta))
+        halves = prob.totals(theta, i1=n // 3) + prob.totals(theta, i0=n // 3)
+        fields_close(halves, whole, 1, 3, 1e-11)
+        P = vo.split_acc(whole, 1, 3)
+        assert P["dlogdet"][0] == pytest.approx(n / theta[0], rel=1e-10)
+        assert P["ainfo"][0, 0] == pytest.approx(0.5 * n / theta[0] ** 2, rel=1e-10)
+        k = 1 << 14
+        want = vo.run(y, X, locs, nn.idx, "matern15_isotropic", theta, i0=0, i1=k)
+        fields_close(prob.totals(theta, i0=0, i1=k), want, 1, 3, 1e-9)

@@ -1,0 +1,275 @@
+"""CPU-side tests: host logic of the fitting API, the C ABI surface, and the multi-rank
+combine step under gloo.  No compute call reaches the GPU library here."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2407_02740_b200 as vg
+from paper_2407_02740_b200 import _cabi, build, distributed, engine, inference
+from oracle import vecchia_oracle as vo
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+# ---- C ABI -------------------------------------------------------------------
+def test_library_builds_and_exports_every_declared_symbol():
+    lib_path = build.build_cuda()
+    assert lib_path.exists()
+    header = (ROOT / "include" / "vecchia_b200.h").read_text()
+    declared = set(re.findall(r"\b(vb200_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations found"
+    lib = ctypes.CDLL(str(lib_path))
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in include/vecchia_b200.h but not exported"
+    assert set(_cabi.EXPORTED_SYMBOLS) == declared
+    L = _cabi.load()
+    assert L.vb200_abi_version() == 1
+    assert L.vb200_acc_len(1, 3) == 25 and L.vb200_acc_len(4, 3) == 97 and L.vb200_acc_len(1, 4) == 36
+    assert L.vb200_family_nparms(0, 2) == 3 and L.vb200_family_nparms(1, 3) == 5
+    assert L.vb200_family_nparms(2, 3) == 4 and L.vb200_family_nparms(9, 2) < 0
+
+
+def test_sass_is_sm100a_fp64():
+    out = subprocess.run(["cuobjdump", "-lelf", str(build.build_cuda())], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.skipif(_cabi.device_count() > 0, reason="a GPU is present")
+def test_no_cpu_fallback_without_device():
+    ds = vg.Dataset(np.zeros(4), np.ones((4, 1)), np.arange(8.0).reshape(4, 2))
+    nn = vg.find_ordered_neighbors(ds.locs, 2)
+    with pytest.raises(vg.DeviceUnavailable):
+        engine.run(ds, nn, vg.CovarianceParameters("exponential_isotropic", [1.0, 0.5, 0.1]))
+    handle = ctypes.c_void_p()
+    y = np.zeros(4)
+    rc = _cabi.load().vb200_create(0, 4, 1, 2, 3, y.ctypes.data, y.ctypes.data, y.ctypes.data, y.ctypes.data, 0, 4,
+                                   None, ctypes.byref(handle))
+    assert rc == _cabi.VB200_ECUDA and "no CPU fallback" in _cabi.last_error()
+
+
+def test_product_never_imports_the_oracle():
+    for path in (ROOT / "paper_2407_02740_b200").rglob("*.py"):
+        text = path.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, path
+    for path in (ROOT / "paper_2407_02740_b200" / "csrc").glob("*"):
+        assert "oracle" not in path.read_text().lower() or path.suffix == ".md", path
+
+
+# ---- model / covariance / preprocess ------------------------------------------
+def test_model_types_and_validation():
+    ds = vg.Dataset([1, 2, 3], [1, 1, 1], [[0, 0], [1, 0], [0, 1]])
+    assert ds.n == 3 and ds.p == 1 and ds.d == 2 and ds.X.dtype == np.float64
+    vg.validate_dataset(ds)
+    with pytest.raises(vg.EmptyData):
+        vg.validate_dataset(vg.Dataset([], np.zeros((0, 1)), np.zeros((0, 2))))
+    with pytest.raises(vg.DimensionMismatch):
+        vg.validate_dataset(vg.Dataset([1, 2], np.ones((3, 1)), np.zeros((3, 2))))
+    with pytest.raises(vg.NonFiniteValue):
+        vg.validate_dataset(vg.Dataset([1, np.nan], np.ones((2, 1)), np.zeros((2, 2))))
+    assert vg.normalize_backend("seq") == "sequential" and vg.normalize_backend("staged-batched") == "staged"
+    with pytest.raises(ValueError):
+        vg.normalize_backend("gpu")
+    with pytest.raises(ValueError):
+        vg.ModelSpec(vg.CovarianceParameters("exponential_isotropic", [1, 1, 0]), m=0)
+    assert engine.choose_capacity_tier(31) == 32 and engine.choose_capacity_tier(80) == 80
+    assert engine.available_cores() == ("cuda",) and engine.active_core_name() == "cuda"
+
+
+def test_covariance_registry_known_answers():
+    # e^-1 entries (reference tests/test_covariance.py:26-30, 71-74)
+    fam = vg.covariance_registry("exponential_isotropic")
+    K = fam.matrix([2.0, 0.5, 0.1], [[0.0, 0.0], [0.5, 0.0]])
+    assert K[0, 1] == pytest.approx(2.0 * np.exp(-1.0)) and K[0, 0] == pytest.approx(2.2)
+    D = fam.derivatives([2.0, 0.5, 0.1], [[0.0, 0.0], [0.5, 0.0]])
+    assert D[0][0, 1] == pytest.approx(np.exp(-1.0)) and D[1][0, 1] == pytest.approx(2 * np.exp(-1.0) * 0.5 / 0.25)
+    assert np.array_equal(D[2], 2.0 * np.eye(2)) and D[1][0, 0] == 0.0
+    with pytest.raises(vg.UnknownFamily):
+        vg.covariance_registry("matern")
+    with pytest.raises(ValueError):
+        vg.validate_parameters(vg.CovarianceParameters("exponential_anisotropic", [1, 1, 0]), 2)
+    with pytest.raises(ValueError):
+        vg.validate_parameters(vg.CovarianceParameters("exponential_isotropic", [1, 0.0, 0]), 2)
+    with pytest.raises(ValueError):
+        vg.validate_parameters(vg.CovarianceParameters("exponential_isotropic", [1, 1, -0.1]), 2)
+    assert vg.covariance_registry("exponential_spacetime").nparms(3) == 4
+    assert vg.covariance_registry("exponential_anisotropic").nparms(3) == 5
+
+
+@pytest.mark.parametrize("family,d,theta", [
+    ("exponential_isotropic", 2, [1.3, 0.4, 0.2]), ("exponential_anisotropic", 3, [1.3, 0.4, 0.7, 0.2, 0.1]),
+    ("exponential_spacetime", 3, [1.3, 0.4, 0.9, 0.1]), ("matern15_isotropic", 2, [0.9, 0.3, 0.05]),
+    ("matern25_isotropic", 2, [0.9, 0.3, 0.05])])
+def test_covariance_derivatives_vs_finite_differences(family, d, theta):
+    from oracle import numpy_families
+    rng = np.random.default_rng(1)
+    pts = rng.uniform(0, 1, (7, d))
+    fam = vg.covariance_registry(family)
+    theta = np.asarray(theta)
+    D = fam.derivatives(theta, pts)
+    K0, D0 = numpy_families.cov_and_derivs(family, theta, pts)
+    np.testing.assert_allclose(fam.matrix(theta, pts), K0, rtol=1e-13)
+    np.testing.assert_allclose(D, D0, rtol=1e-12, atol=1e-14)
+    for j in range(theta.shape[0]):
+        h = 1e-6 * theta[j]
+        tp, tm = theta.copy(), theta.copy()
+        tp[j] += h
+        tm[j] -= h
+        np.testing.assert_allclose(D[j], (fam.matrix(tp, pts) - fam.matrix(tm, pts)) / (2 * h), rtol=1e-6, atol=1e-8)
+
+
+def test_sphere_embedding_and_orderings():
+    xyz = vg.embed_lonlat([[0.0, 0.0], [90.0, 0.0], [0.0, 90.0]])
+    np.testing.assert_allclose(xyz, [[1, 0, 0], [0, 1, 0], [0, 0, 1]], atol=1e-15)
+    with pytest.raises(vg.LatitudeOutOfRange):
+        vg.embed_lonlat([[0.0, 91.0]])
+    with pytest.raises(vg.LatitudeOutOfRange):
+        vg.lonlat_to_xyz(0.0, -90.5)
+    perm = vg.random_permutation(10, 5).perm
+    assert sorted(perm) == list(range(10))
+    assert np.array_equal(perm, np.random.Generator(np.random.PCG64(5)).permutation(10))
+    ds = vg.Dataset(np.arange(10.0), np.ones(10), np.arange(20.0).reshape(10, 2))
+    re_ds = vg.reorder_dataset(ds, vg.Ordering(perm))
+    assert np.array_equal(re_ds.y, ds.y[perm]) and np.array_equal(re_ds.locs, ds.locs[perm])
+    with pytest.raises(vg.LengthMismatch):
+        vg.reorder_dataset(ds, vg.identity_ordering(9))
+
+
+@pytest.mark.parametrize("name", ["grid7", "grid3d", "rand2d", "rand3d", "line", "dups"])
+@pytest.mark.parametrize("method", ["exhaustive", "grid"])
+def test_neighbor_table_matches_reference_golden(neighbor_cases, name, method):
+    z = neighbor_cases
+    got = vg.find_ordered_neighbors(z[f"{name}/locs"], int(z[f"{name}/m"]), method=method)
+    assert np.array_equal(got.idx, z[f"{name}/idx"])
+
+
+def test_neighbor_grid_equals_exhaustive_scan_with_ties_and_row_ranges():
+    from paper_2407_02740_b200.preprocess import find_ordered_neighbor_rows
+    rng = np.random.default_rng(12)
+    for n, d, m in [(6000, 2, 30), (5000, 3, 11), (4500, 1, 4), (5000, 5, 9)]:
+        locs = rng.uniform(0, 1, (n, d))
+        a = vg.find_ordered_neighbors(locs, m, method="exhaustive").idx
+        assert np.array_equal(a, vo.neighbor_scan(locs, m))
+        assert np.array_equal(a, vg.find_ordered_neighbors(locs, m, method="grid", workers=3).idx)
+        assert np.array_equal(a[1000:3500], find_ordered_neighbor_rows(locs, m, 1000, 2500))
+    xs, ys = np.meshgrid(np.arange(70.0), np.arange(70.0))
+    g = np.column_stack([xs.ravel(), ys.ravel()])[rng.permutation(4900)]
+    assert np.array_equal(vg.find_ordered_neighbors(g, 12, method="grid").idx, vo.neighbor_scan(g, 12))
+    clustered = np.concatenate([rng.normal(0, 0.01, (3000, 2)), rng.uniform(-5, 5, (2500, 2))])[rng.permutation(5500)]
+    assert np.array_equal(vg.find_ordered_neighbors(clustered, 20, method="grid").idx, vo.neighbor_scan(clustered, 20))
+    tiny = vg.find_ordered_neighbors(np.array([[0.0], [1.0], [2.0], [3.0], [4.0]]), 2)
+    assert np.array_equal(tiny.idx, [[0, -1, -1], [1, 0, -1], [2, 1, 0], [3, 2, 1], [4, 3, 2]])  # test_preprocess.py:124-136
+    assert vg.find_ordered_neighbors(np.zeros((1, 2)), 5).idx.shape == (1, 2)
+
+
+# ---- inference -----------------------------------------------------------------
+def test_fisher_step_known_answers():
+    # reference tests/test_inference.py:84-115
+    step = inference.fisher_step(np.zeros(2), np.array([1.0, 2.0]), np.diag([2.0, 4.0]))
+    np.testing.assert_allclose(step, [0.5, 0.5])
+    assert np.array_equal(inference.fisher_step(np.array([0.3, 0.4]), np.zeros(2), np.eye(2)), [0.3, 0.4])
+    out = inference.fisher_step(np.zeros(2), np.array([1.0, 1.0]), np.zeros((2, 2)))  # needs damping
+    assert np.all(np.isfinite(out)) and out @ np.array([1.0, 1.0]) > 0
+    with pytest.raises(vg.DegenerateInformation):
+        inference.fisher_step(np.zeros(2), np.array([1.0, 1.0]), -10.0 * np.eye(2))
+    g, info = inference.to_log_scale([2.0, 0.5], np.array([1.0, 4.0]), np.array([[1.0, 2.0], [2.0, 8.0]]))
+    np.testing.assert_allclose(g, [2.0, 2.0])
+    np.testing.assert_allclose(info, [[4.0, 2.0], [2.0, 2.0]])
+
+
+def test_assemble_on_reference_totals(engine_cases):
+    for name in engine_cases["names"]:
+        name = str(name)
+        tot = engine_cases[f"{name}/totals_compiled"]
+        p, q = engine_cases[f"{name}/X"].shape[1], engine_cases[f"{name}/theta"].shape[0]
+        parts = engine.parts_from_flat(tot, p, q)
+        assert np.array_equal(engine.flat_from_parts(parts), tot)
+        ev = vg.assemble(parts, engine_cases[f"{name}/y"].shape[0])
+        assert ev.loglik == pytest.approx(float(engine_cases[f"{name}/loglik_compiled"]), rel=1e-13)
+        np.testing.assert_allclose(ev.grad, engine_cases[f"{name}/grad_compiled"], rtol=1e-9, atol=1e-10)
+        np.testing.assert_allclose(ev.beta_hat, engine_cases[f"{name}/beta_compiled"], rtol=1e-10)
+    bad = engine.parts_from_flat(np.zeros(engine.acc_len(2, 3)), 2, 3)
+    with pytest.raises(vg.SingularDesign):
+        vg.assemble(bad, 10)
+
+
+def test_fit_loop_with_cpu_evaluator_reproduces_reference_fit(fit_cases):
+    """The scoring loop (host logic) driven by the ORACLE as evaluator must reproduce the
+    reference's fit exactly -- separates fit-loop parity from kernel parity."""
+    z, tag = fit_cases, "cli300_a"
+    g = lambda k: z[f"{tag}/{k}"]
+    ds = vg.Dataset(g("y"), g("X"), g("locs"))
+    nn = vg.NeighborArray(g("nn"))
+
+    def evaluator(theta):
+        tot = vo.run(ds.y, ds.X, ds.locs, nn.idx, "exponential_isotropic", theta, deterministic=True)
+        return vg.assemble(engine.parts_from_flat(tot, ds.p, 3), ds.n)
+
+    start = vg.default_start(ds, "exponential_isotropic")
+    np.testing.assert_allclose(start.theta, g("start"), rtol=1e-14)
+    res = vg.fit(ds, nn, vg.ModelSpec(covariance=start, m=int(g("m"))), evaluator=evaluator)
+    np.testing.assert_allclose(res.theta_hat.theta, g("compiled/theta_hat"), rtol=1e-12)
+    np.testing.assert_allclose(res.loglik_trace, g("compiled/trace"), rtol=1e-13)
+    assert res.iterations == int(g("compiled/iterations")) and res.converged
+    assert res.loglik == pytest.approx(-398.7845764605893, rel=1e-12)  # pkg/test_output.txt:36
+
+
+# ---- multi-rank combine (gloo, world_size 2) ------------------------------------
+def test_shard_bounds_cover_range():
+    for n, w in [(10, 3), (1 << 20, 8), (5, 8), (0, 2)]:
+        cuts = [distributed.shard_bounds(n, w, r) for r in range(w)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+        assert max(b - a for a, b in cuts) - min(b - a for a, b in cuts) <= 1
+
+
+_WORKER = r"""
+import os, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+from paper_2407_02740_b200 import distributed
+from oracle import vecchia_oracle as vo
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+rng = np.random.default_rng(3)
+n, m = 600, 8
+locs = rng.uniform(0, 1, (n, 2)); y = rng.normal(size=n); X = np.ones((n, 1))
+nn = vo.neighbor_scan(locs, m)
+theta = np.array([1.2, 0.3, 0.1])
+i0, i1 = distributed.shard_bounds(n, world, rank)
+# each rank's (L+2,) vector in the layout of vb200_eval_async, produced here by the CPU oracle
+local = vo.run(y, X, locs, nn, "exponential_isotropic", theta, i0=i0, i1=i1)
+vec = torch.from_numpy(np.concatenate([local, [0.0, -np.inf]]))
+tot, first = distributed.combine_partials(vec)
+whole = vo.run(y, X, locs, nn, "exponential_isotropic", theta)
+assert first == -1
+np.testing.assert_allclose(tot, whole, rtol=1e-12, atol=1e-12)
+# failure on the last rank only: every rank must learn the lowest failing index
+fail = torch.from_numpy(np.concatenate([local, [2.0 if rank == world - 1 else 0.0,
+                                                -(i0 + 5.0) - 1.0 if rank == world - 1 else -np.inf]]))
+tot, first = distributed.combine_partials(fail)
+lo = distributed.shard_bounds(n, world, world - 1)[0]
+assert first == lo + 5, (first, lo)
+dist.destroy_process_group()
+print("rank", rank, "ok")
+"""
+
+
+def test_combine_partials_world_size_2_gloo(tmp_path):
+    script = tmp_path / "worker.py"
+    script.write_text(_WORKER.format(root=str(ROOT)))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", WORLD_SIZE="2", OMP_NUM_THREADS="2")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=240)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o
