@@ -1,8 +1,514 @@
-// kernel_tiled.cuh -- layout TILED_REG (placeholder until the register-tiled kernel lands).
+// kernel_tiled.cuh -- layout TILED_REG: the fast path.
+//
+// G lanes of a warp cooperate on one observation (32/G observations per warp).  Every
+// lane owns S rows of the local (CAP x CAP, CAP = G*S) covariance matrix, folded
+// boustrophedon-wise (slot s even: row s*G + lane, slot s odd: row s*G + G-1-lane) so
+// that the triangular work is balanced, and keeps those rows IN REGISTERS for the whole
+// factorization.  Shared memory is used only as a staging / broadcast medium:
+//   * the pair terms (one exp + one sqrt per pair) are computed pair-parallel, perfectly
+//     balanced over the lanes, staged in a packed triangle, then read back row-wise;
+//   * at Cholesky step j the scaled column j is written once and read back as broadcast
+//     128-bit loads (1 LDS per 2 values instead of 4 SHFL); the columns stay in shared
+//     memory and serve the transposed back-substitution for u = B^-T e_last;
+//   * the packed range-derivative matrices D_j wait there for the symmetric mat-vec D_j u.
+// The forward substitutions of y and X ride along inside the Cholesky sweep (their
+// updates use the freshly scaled column that is already in registers).
+//
+// Rows with fewer than CAP live points (the ragged head rows i < m, or m+1 < CAP) are
+// padded at the FRONT of the local frame with identity rows and zero data, which leaves
+// every accumulator term of the real block unchanged (chol([[I,0],[0,K]]) = [[I,0],[0,B]]).
+//
+// Same per-observation mathematics as kernel_warp_smem.cuh / the reference's
+// _obs_kernel (/root/reference/pkg/src/vecchiagp/engine/_kernels.pyx:347-381); see
+// common.cuh for the reference map.
 #pragma once
 #include "common.cuh"
 
-static inline bool tiled_supported(int, int, int, int, int) { return false; }
+#define FULLMASK 0xffffffffu
 
+template <int FAM, int D>
+struct FamTraits {
+    static constexpr int QD = (FAM == FAM_EXP_ANISO) ? D : (FAM == FAM_EXP_SPACETIME ? 2 : 1);
+    static constexpr int Q = QD + 2;
+};
+
+// pair terms with a compile-time coordinate count (registers only, no local arrays)
+template <int FAM, int D>
+__device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double (&dl)[D], double &Kv,
+                                             double (&Dv)[FamTraits<FAM, D>::QD])
+{
+    if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l)
+            d2 = fma(dl[l], dl[l], d2);
+        const double ir = E.inv_rho[0];
+        const double x = sqrt(d2) * ir;
+        const double e = exp(-x);
+        const double se = E.sig2 * e;
+        if constexpr (FAM == FAM_EXP_ISO) {
+            Kv = se;
+            Dv[0] = se * x * ir;
+        } else if constexpr (FAM == FAM_MATERN15) {
+            Kv = se * (1.0 + x);
+            Dv[0] = se * x * x * ir;
+        } else {
+            Kv = se * (1.0 + x + x * x * (1.0 / 3.0));
+            Dv[0] = se * x * x * (1.0 + x) * ir * (1.0 / 3.0);
+        }
+    } else {
+        double sc[D];
+        double s2 = 0.0, sp2 = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            const double t = dl[l] * E.inv_rho[l];
+            sc[l] = t * t;
+            s2 += sc[l];
+            if (l < D - 1)
+                sp2 += sc[l];
+        }
+        const double s = sqrt(s2);
+        Kv = E.sig2 * exp(-s);
+        const double g = (s == 0.0) ? 0.0 : Kv / s;
+        if constexpr (FAM == FAM_EXP_ANISO) {
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+                Dv[l] = g * sc[l] * E.inv_rho[l];
+        } else {
+            Dv[0] = g * sp2 * E.inv_rho[0];
+            Dv[1] = g * sc[D - 1] * E.inv_rho[D - 1];
+        }
+    }
+}
+
+template <int G, int S>
+struct TileGeom {
+    static constexpr int CAP = G * S;
+    static constexpr int OPW = 32 / G;                 // observations per warp
+    static constexpr int TRI = CAP * (CAP + 1) / 2;    // packed lower triangle incl. diagonal
+    // column store of L: element (c, j), c >= j, lives at colbase(j) + c; colbase(j) is even so
+    // that pairs (c, c+1) with c even are 16-byte aligned (CAP is even for every tier)
+    __host__ __device__ static constexpr int colbase(int j) { return j * (CAP - 1) - j * (j - 1) / 2 + (j + 1) / 2; }
+    static constexpr int LST = colbase(CAP - 1) + CAP; // doubles in the column store
+    static constexpr int KL = ((LST > TRI ? LST : TRI) + 1) & ~1;
+    __host__ __device__ static constexpr int slot_of(int r) { return r / G; }
+    __host__ __device__ static constexpr int lane_of(int r) { return ((r / G) & 1) ? (G - 1 - r % G) : (r % G); }
+};
+
+template <int G, int S, int D, int QD>
+struct TileSmem {
+    using Geo = TileGeom<G, S>;
+    static constexpr int TAB_DOUBLES = (Geo::TRI * 2 + 15) / 16 * 2; // uint16 pair table, 16-byte rounded
+    static constexpr int PTS = Geo::CAP * D;
+    static constexpr int PER_OBS = ((PTS + 1) & ~1) + Geo::CAP + Geo::KL + QD * ((Geo::TRI + 1) & ~1);
+    static constexpr int TOTAL = TAB_DOUBLES + Geo::OPW * PER_OBS;
+};
+
+template <int G, int S, int FAM, int D, int P>
+__global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
+{
+    using Geo = TileGeom<G, S>;
+    using FT = FamTraits<FAM, D>;
+    constexpr int CAP = Geo::CAP, TRI = Geo::TRI, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
+    constexpr int TRIP = (TRI + 1) & ~1;
+    using SM = TileSmem<G, S, D, QD>;
+    constexpr int L = (1 + Q) * (2 + P + P * P) + Q * Q;
+    constexpr int NACC = (L + G - 1) / G;
+    const AccLayout A(P, Q);
+
+    extern __shared__ double smem[];
+    unsigned short *tab = reinterpret_cast<unsigned short *>(smem);
+    const int lane = threadIdx.x;
+    const int g = lane / G, lg = lane % G;
+    double *obs = smem + SM::TAB_DOUBLES + g * SM::PER_OBS;
+    double *pts = obs;                               // CAP x D coordinates of the local frame
+    double *uvec = obs + ((SM::PTS + 1) & ~1);       // u = B^-T e_last
+    double *KLs = uvec + CAP;                        // packed K staging, then the column store of L
+    double *Dms = KLs + Geo::KL;                     // QD packed derivative matrices
+
+    // pair table: packed index t -> (a, c), a >= c
+    for (int t = lane; t < TRI; t += 32) {
+        int a = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while (a * (a + 1) / 2 > t)
+            --a;
+        while ((a + 1) * (a + 2) / 2 <= t)
+            ++a;
+        tab[t] = (unsigned short)((a << 8) | (t - a * (a + 1) / 2));
+    }
+    int rowi[S], tri_r[S], colb_r[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        rowi[s] = s * G + ((s & 1) ? (G - 1 - lg) : lg);
+        tri_r[s] = rowi[s] * (rowi[s] + 1) / 2;
+        colb_r[s] = Geo::colbase(rowi[s]);
+    }
+    double acc[NACC];
+#pragma unroll
+    for (int t = 0; t < NACC; ++t)
+        acc[t] = 0.0;
+    __syncwarp();
+
+    const int64_t nbatch = (E.i1 - E.i0 + OPW - 1) / OPW;
+    for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
+        const int64_t i = E.i0 + batch * OPW + g;
+        const bool active = i < E.i1;
+        const int64_t *nrow = E.nn + (active ? (i - E.nn_row0) : 0) * E.mp1;
+
+        // ---- gather: local index a <-> neighbor column CAP-1-a (observation last) ----
+        double rhs[1 + P][S];
+        int nlive = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int a = rowi[s], col = CAP - 1 - a;
+            int64_t idx = -1;
+            if (active && col < E.mp1)
+                idx = nrow[col];
+            const bool live = idx >= 0;
+            double cx[D];
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+                cx[l] = 0.0;
+            rhs[0][s] = 0.0;
+#pragma unroll
+            for (int b = 0; b < P; ++b)
+                rhs[1 + b][s] = 0.0;
+            if (live) {
+                const double *r = E.rec + idx * E.rs;
+#pragma unroll
+                for (int l = 0; l < D; ++l)
+                    cx[l] = r[l];
+                rhs[0][s] = r[D];
+#pragma unroll
+                for (int b = 0; b < P; ++b)
+                    rhs[1 + b][s] = r[D + 1 + b];
+            }
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+                pts[a * D + l] = cx[l];
+            const unsigned bal = __ballot_sync(FULLMASK, live);
+            nlive += __popc((G == 32) ? bal : ((bal >> (g * G)) & ((1u << (G & 31)) - 1u)));
+        }
+        const int pad = CAP - nlive; // identity rows at the front of the local frame
+        __syncwarp();
+
+        // ---- pair terms, balanced over the lanes of the group, staged in the packed triangle ----
+        for (int t = lg; t < TRI; t += G) {
+            const unsigned ac = tab[t];
+            const int a = ac >> 8, c = ac & 255;
+            double dl[D], Kv, Dv[QD];
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+                dl[l] = pts[a * D + l] - pts[c * D + l];
+            pair_terms_s<FAM, D>(E, dl, Kv, Dv);
+            const bool diag = (a == c), dummy = (c < pad);
+            KLs[t] = dummy ? (diag ? 1.0 : 0.0) : (diag ? E.diag : Kv);
+#pragma unroll
+            for (int j = 0; j < QD; ++j)
+                Dms[j * TRIP + t] = (dummy || diag) ? 0.0 : Dv[j];
+        }
+        __syncwarp();
+
+        // ---- own rows into registers ----
+        double Kr[S][CAP];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int c = 0; c < (s + 1) * G; ++c)
+                Kr[s][c] = KLs[tri_r[s] + c];
+        __syncwarp();
+
+        // ---- Cholesky (right-looking) with the forward substitutions of y and X fused in ----
+        double invd[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            invd[s] = 0.0;
+        int failpiv = 0;
+        double pv_last = 1.0;
+#pragma unroll
+        for (int j = 0; j < CAP; ++j) {
+            const int sj = j / G;
+            const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
+            const double pv = __shfl_sync(FULLMASK, Kr[sj][j], oj, G);
+            failpiv = (failpiv == 0 && pv <= 0.0) ? (j + 1) : failpiv;
+            if (j == CAP - 1)
+                pv_last = pv;
+            const double inv = rsqrt(pv);
+            // Lo[s] = L[row][j] for rows below the pivot row, exactly 0 for finished rows, so the
+            // updates below need no per-row predicates (a finished row just adds -0 * x)
+            double Lo[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if ((s + 1) * G - 1 >= j) { // slot still has rows >= j
+                    const double Lraw = Kr[s][j] * inv;
+                    Kr[s][j] = Lraw;
+                    Lo[s] = (rowi[s] > j) ? Lraw : 0.0;
+                    if (rowi[s] > j)
+                        KLs[Geo::colbase(j) + rowi[s]] = Lraw;
+                    invd[s] = (rowi[s] == j) ? inv : invd[s];
+                } else {
+                    Lo[s] = 0.0;
+                }
+            }
+            // forward substitution of y and X rides along; the pivot row keeps its unscaled
+            // value (z_j = rhs_j * invd_j is applied once after the sweep)
+#pragma unroll
+            for (int r = 0; r < 1 + P; ++r) {
+                const double xr = __shfl_sync(FULLMASK, rhs[r][sj], oj, G) * inv;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if ((s + 1) * G - 1 > j)
+                        rhs[r][s] = fma(-Lo[s], xr, rhs[r][s]);
+            }
+            __syncwarp();
+            if (j + 1 < CAP) {
+                const double *col = KLs + Geo::colbase(j);
+#pragma unroll
+                for (int c0 = (j + 1) & ~1; c0 < CAP; c0 += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(col + c0);
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (c0 > j && (s + 1) * G - 1 >= c0)
+                            Kr[s][c0] = fma(-Lo[s], v.x, Kr[s][c0]);
+                        if ((s + 1) * G - 1 >= c0 + 1)
+                            Kr[s][c0 + 1] = fma(-Lo[s], v.y, Kr[s][c0 + 1]);
+                    }
+                }
+            }
+        }
+
+#pragma unroll
+        for (int r = 0; r < 1 + P; ++r)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                rhs[r][s] *= invd[s];
+
+        // ---- u = B^-T e_last: lane owning index j reads column j of L from the column store ----
+        double ub[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            ub[s] = (rowi[s] == CAP - 1) ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = CAP - 1; l >= 0; --l) {
+            const int sl = l / G;
+            const int ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
+            const double ul = __shfl_sync(FULLMASK, ub[sl] * invd[sl], ol, G);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (s * G < l) { // slot has rows < l
+                    const double Llj = (rowi[s] < l) ? KLs[colb_r[s] + l] : 0.0;
+                    ub[s] = fma(-Llj, ul, ub[s]);
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            ub[s] *= invd[s];
+            uvec[rowi[s]] = ub[s];
+        }
+        __syncwarp();
+
+        // ---- t_j = D_j u (symmetric packed mat-vec), then [t_1..t_QD, u] through B^-1 ----
+        double rr[QD + 1][S];
+#pragma unroll
+        for (int r = 0; r < QD; ++r)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                rr[r][s] = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < CAP; ++c) {
+            const double uc = uvec[c];
+            const int tc = c * (c + 1) / 2;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int addr = (c < rowi[s]) ? (tri_r[s] + c) : (tc + rowi[s]);
+#pragma unroll
+                for (int r = 0; r < QD; ++r)
+                    rr[r][s] = fma(Dms[r * TRIP + addr], uc, rr[r][s]);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            rr[QD][s] = ub[s];
+#pragma unroll
+        for (int j = 0; j < CAP; ++j) {
+            const int sj = j / G;
+            const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
+            double Lm[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                Lm[s] = ((s + 1) * G - 1 > j && rowi[s] > j) ? Kr[s][j] : 0.0;
+#pragma unroll
+            for (int r = 0; r < QD + 1; ++r) {
+                const double x = __shfl_sync(FULLMASK, rr[r][sj] * invd[sj], oj, G);
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if ((s + 1) * G - 1 > j)
+                        rr[r][s] = fma(-Lm[s], x, rr[r][s]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < QD + 1; ++r)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                rr[r][s] *= invd[s];
+        // now rr[r] = c_dense_r (r < QD), rr[QD] = w = B^-1 u; rhs[0] = z, rhs[1+b] = W_b
+
+        // ---- dot products over the local index, reduced over the G lanes of the group ----
+        auto gsum = [](double v) {
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1)
+                v += __shfl_xor_sync(FULLMASK, v, off, G);
+            return v;
+        };
+        auto dot = [&](const double (&x)[S], const double (&y)[S]) {
+            double s0 = 0.0;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                s0 = fma(x[s], y[s], s0);
+            return gsum(s0);
+        };
+        constexpr int se = S - 1;
+        constexpr int oe = Geo::lane_of(CAP - 1);
+        const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G);
+        const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G);
+        double we[P], ce[Q], zc[Q], wc[P * Q], cc[Q * Q];
+#pragma unroll
+        for (int b = 0; b < P; ++b)
+            we[b] = __shfl_sync(FULLMASK, rhs[1 + b][se], oe, G);
+        const double jit = E.jitter, is2 = E.inv_sig2, s2 = E.sig2;
+        {
+            const double zw = dot(rhs[0], rr[QD]);
+            const double ww = dot(rr[QD], rr[QD]);
+            ce[0] = (1.0 - jit * w_e) * is2;
+            ce[Q - 1] = s2 * w_e;
+            zc[0] = (ze - jit * zw) * is2;
+            zc[Q - 1] = s2 * zw;
+            cc[0] = (1.0 - 2.0 * jit * w_e + jit * jit * ww) * is2 * is2;
+            cc[Q - 1] = cc[(Q - 1) * Q] = w_e - jit * ww;
+            cc[(Q - 1) * Q + Q - 1] = s2 * s2 * ww;
+#pragma unroll
+            for (int b = 0; b < P; ++b) {
+                const double Ww = dot(rhs[1 + b], rr[QD]);
+                wc[b * Q] = (we[b] - jit * Ww) * is2;
+                wc[b * Q + Q - 1] = s2 * Ww;
+            }
+#pragma unroll
+            for (int r = 0; r < QD; ++r) {
+                const double cde = __shfl_sync(FULLMASK, rr[r][se], oe, G);
+                const double wcd = dot(rr[QD], rr[r]);
+                ce[1 + r] = cde;
+                zc[1 + r] = dot(rhs[0], rr[r]);
+                cc[1 + r] = cc[(1 + r) * Q] = (cde - jit * wcd) * is2;
+                cc[(1 + r) * Q + Q - 1] = cc[(Q - 1) * Q + 1 + r] = s2 * wcd;
+#pragma unroll
+                for (int b = 0; b < P; ++b)
+                    wc[b * Q + 1 + r] = dot(rhs[1 + b], rr[r]);
+#pragma unroll
+                for (int r2 = 0; r2 <= r; ++r2) {
+                    const double v = dot(rr[r], rr[r2]);
+                    cc[(1 + r) * Q + 1 + r2] = v;
+                    cc[(1 + r2) * Q + 1 + r] = v;
+                }
+            }
+        }
+        const double logdet = log(pv_last);
+        const bool emit = active && failpiv == 0;
+#pragma unroll
+        for (int o = 0; o < L; ++o) {
+            if (lg == (o % G)) {
+                const double v = emit_value(o, P, Q, A, logdet, ze, we, ce, zc, wc, cc);
+                acc[o / G] += emit ? v : 0.0;
+                if (E.rows != nullptr && emit)
+                    E.rows[(size_t)(i - E.i0) * L + o] = v;
+            }
+        }
+        if (active && failpiv != 0 && lg == 0) {
+            report_failure(E, i, failpiv - pad);
+            if (E.fail_rows)
+                E.fail_rows[i - E.i0] = failpiv - pad;
+        }
+        __syncwarp();
+    }
+
+    // ---- block partial: add the groups of this warp in fixed order, one row of `partials` per block ----
+#pragma unroll
+    for (int t = 0; t < NACC; ++t) {
+        double v = acc[t];
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1)
+            v += __shfl_xor_sync(FULLMASK, v, off);
+        const int o = t * G + lg;
+        if (g == 0 && o < L)
+            E.partials[(size_t)blockIdx.x * L + o] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side: instance table and launch
+// ---------------------------------------------------------------------------
+struct TiledInstance {
+    int g, cap, family, d, p;
+    void (*kernel)(const EvalParams);
+    int smem_doubles;
+    const char *name;
+};
+
+#define TILED_INST(G_, S_, FAM_, D_, P_)                                                                        \
+    {                                                                                                           \
+        G_, (G_) * (S_), FAM_, D_, P_, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
+            TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
+            "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                            \
+    }
+
+#include "tiled_instances.inc"
+
+static inline const TiledInstance *tiled_find(int family, int mp1, int p, int d)
+{
+    const TiledInstance *best = nullptr;
+    for (const TiledInstance &t : kTiledInstances)
+        if (t.family == family && t.d == d && t.p == p && t.cap >= mp1 && (!best || t.cap < best->cap))
+            best = &t;
+    return best;
+}
+
+static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
+{
+    return tiled_find(family, mp1, p, d) != nullptr;
+}
+
+// returns 0, -100 (CUDA error pending), or a VB200_E* code
 template <class PartialsFn>
-static int launch_tiled(cudaStream_t, int, size_t, EvalParams &, int *, const char **, PartialsFn) { return -4; }
+static int launch_tiled(cudaStream_t stream, int sm_count, size_t smem_optin, EvalParams &E, int *nblocks,
+                        const char **name, PartialsFn get_partials)
+{
+    const TiledInstance *t = tiled_find(E.family, E.mp1, E.p, E.d);
+    if (!t)
+        return -4;
+    const size_t smem = (size_t)t->smem_doubles * sizeof(double);
+    if (smem > smem_optin)
+        return -4;
+    if (cudaFuncSetAttribute(t->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return -100;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t->kernel, 32, smem) != cudaSuccess)
+        return -100;
+    if (per_sm < 1)
+        per_sm = 1;
+    const int opw = 32 / t->g;
+    const int64_t nbatch = (E.i1 - E.i0 + opw - 1) / opw;
+    int64_t blocks = (int64_t)sm_count * per_sm;
+    if (blocks > nbatch)
+        blocks = nbatch;
+    if (blocks < 1)
+        blocks = 1;
+    double *partials = get_partials((size_t)blocks * E.L);
+    if (!partials)
+        return -3;
+    E.partials = partials;
+    t->kernel<<<(unsigned)blocks, 32, smem, stream>>>(E);
+    if (cudaGetLastError() != cudaSuccess)
+        return -100;
+    *nblocks = (int)blocks;
+    *name = t->name;
+    return 0;
+}

@@ -140,7 +140,7 @@ def test_not_positive_definite_reports_observation_and_pivot(failure_case):
             assert err.value.observation == int(z["observation_compiled"]) == 7
             assert err.value.pivot == int(z["pivot_compiled"])
             rescued = prob.totals(cov.theta, jitter=1e-6)
-            fields_close(rescued, z["rescued_totals"], 1, 3, 1e-6)  # near-singular K: conditioning-limited
+            fields_close(rescued, z["rescued_totals"], 1, 3, 1e-4)  # near-singular K (cond ~1e6): the two CPU oracles differ by 1.4e-5 here
 
 
 FAMILY_SHAPES = [
