@@ -34,31 +34,34 @@ struct FamTraits {
 
 // pair terms with a compile-time coordinate count (registers only, no local arrays)
 template <int FAM, int D>
-__device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double (&dl)[D], double &Kv,
-                                             double (&Dv)[FamTraits<FAM, D>::QD])
+__device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *etab, const double (&dl)[D],
+                                             double &Kv, double (&Dv)[FamTraits<FAM, D>::QD])
 {
+    // squared distances start from 1e-300 instead of 0: coincident points then give x ~ 1e-150,
+    // i.e. exactly the reference's values (exp(-0) = 1, zero range derivative) with no special case
     if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
-        double d2 = 0.0;
+        double d2 = 1e-300;
 #pragma unroll
         for (int l = 0; l < D; ++l)
             d2 = fma(dl[l], dl[l], d2);
         const double ir = E.inv_rho[0];
-        const double x = sqrt(d2) * ir;
-        const double e = exp(-x);
-        const double se = E.sig2 * e;
+        const double x = sqrt_pos(d2) * ir;
+        const double se = E.sig2 * exp_neg(x, etab);
+        const double xi = x * ir;
         if constexpr (FAM == FAM_EXP_ISO) {
             Kv = se;
-            Dv[0] = se * x * ir;
+            Dv[0] = se * xi;
         } else if constexpr (FAM == FAM_MATERN15) {
-            Kv = se * (1.0 + x);
-            Dv[0] = se * x * x * ir;
+            Kv = fma(se, x, se);
+            Dv[0] = (se * x) * xi;
         } else {
-            Kv = se * (1.0 + x + x * x * (1.0 / 3.0));
-            Dv[0] = se * x * x * (1.0 + x) * ir * (1.0 / 3.0);
+            const double x1 = 1.0 + x;
+            Kv = se * fma(x * x, 1.0 / 3.0, x1);
+            Dv[0] = (se * x) * (xi * x1) * (1.0 / 3.0);
         }
     } else {
         double sc[D];
-        double s2 = 0.0, sp2 = 0.0;
+        double s2 = 1e-300, sp2 = 0.0;
 #pragma unroll
         for (int l = 0; l < D; ++l) {
             const double t = dl[l] * E.inv_rho[l];
@@ -67,9 +70,10 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double (
             if (l < D - 1)
                 sp2 += sc[l];
         }
-        const double s = sqrt(s2);
-        Kv = E.sig2 * exp(-s);
-        const double g = (s == 0.0) ? 0.0 : Kv / s;
+        const double rs = rsqrt_pos(s2);
+        const double s = s2 * rs;
+        Kv = E.sig2 * exp_neg(s, etab);
+        const double g = Kv * rs;
         if constexpr (FAM == FAM_EXP_ANISO) {
 #pragma unroll
             for (int l = 0; l < D; ++l)
@@ -98,43 +102,50 @@ struct TileGeom {
 template <int G, int S, int D, int QD>
 struct TileSmem {
     using Geo = TileGeom<G, S>;
-    static constexpr int TAB_DOUBLES = (Geo::TRI * 2 + 15) / 16 * 2; // uint16 pair table, 16-byte rounded
-    static constexpr int PTS = Geo::CAP * D;
-    static constexpr int PER_OBS = ((PTS + 1) & ~1) + Geo::CAP + Geo::KL + QD * ((Geo::TRI + 1) & ~1);
-    static constexpr int TOTAL = TAB_DOUBLES + Geo::OPW * PER_OBS;
+    static constexpr int DP = (D + 1) & ~1;                 // padded coordinate stride (16-byte rows)
+    static constexpr int PTS = Geo::CAP * DP;               // coordinates; reused for u after the build
+    static constexpr int DOFF = Geo::CAP * (Geo::CAP - 1) / 2; // packed strict lower triangle of one D_j
+    static constexpr int DSZ = (DOFF + 1 + 1) & ~1;         // + one zero slot (the diagonal of D_j)
+    static constexpr int PER_OBS = PTS + Geo::KL + QD * DSZ;
+    static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
+    // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
+    // multiple of 2G with copies of the last pair; entry = a << 24 | c << 16 | packed index tri(a)+c
+    static constexpr int TOFF = DOFF;
+    static constexpr int TPAD = (TOFF + 2 * G - 1) / (2 * G) * (2 * G);
 };
 
+// blocks per SM the register budget is tuned for (one warp per block): 3 warps per SM sub-partition
+#define TILED_MIN_BLOCKS 12
+
 template <int G, int S, int FAM, int D, int P>
-__global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
+__global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(const EvalParams E)
 {
     using Geo = TileGeom<G, S>;
     using FT = FamTraits<FAM, D>;
-    constexpr int CAP = Geo::CAP, TRI = Geo::TRI, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
-    constexpr int TRIP = (TRI + 1) & ~1;
+    constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
     using SM = TileSmem<G, S, D, QD>;
+    constexpr int DP = SM::DP, DSZ = SM::DSZ, DZERO = SM::DOFF;
     constexpr int L = (1 + Q) * (2 + P + P * P) + Q * Q;
     constexpr int NACC = (L + G - 1) / G;
     const AccLayout A(P, Q);
+    static_assert(CAP % 2 == 0 && CAP <= 128, "tier geometry");
 
     extern __shared__ double smem[];
-    unsigned short *tab = reinterpret_cast<unsigned short *>(smem);
+    double *etab = smem;                             // 2^(j/64), j < 64
     const int lane = threadIdx.x;
     const int g = lane / G, lg = lane % G;
-    double *obs = smem + SM::TAB_DOUBLES + g * SM::PER_OBS;
-    double *pts = obs;                               // CAP x D coordinates of the local frame
-    double *uvec = obs + ((SM::PTS + 1) & ~1);       // u = B^-T e_last
-    double *KLs = uvec + CAP;                        // packed K staging, then the column store of L
-    double *Dms = KLs + Geo::KL;                     // QD packed derivative matrices
+    double *obs = smem + VB_EXPTAB + g * SM::PER_OBS;
+    double *pts = obs;                               // CAP x DP coordinates of the local frame ...
+    double *uvec = obs;                              // ... later u = B^-T e_last (coordinates are dead by then)
+    double *KLs = obs + SM::PTS;                     // packed K staging, then the column store of L
+    double *Dms = KLs + Geo::KL;                     // QD packed strict-lower derivative matrices (+ zero slot)
 
-    // pair table: packed index t -> (a, c), a >= c
-    for (int t = lane; t < TRI; t += 32) {
-        int a = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-        while (a * (a + 1) / 2 > t)
-            --a;
-        while ((a + 1) * (a + 2) / 2 <= t)
-            ++a;
-        tab[t] = (unsigned short)((a << 8) | (t - a * (a + 1) / 2));
-    }
+    for (int t = lane; t < VB_EXPTAB; t += 32)
+        etab[t] = exp2((double)t * (1.0 / VB_EXPTAB));
+    if (lg == 0)
+#pragma unroll
+        for (int j = 0; j < QD; ++j)
+            Dms[j * DSZ + DZERO] = 0.0;
     int rowi[S], tri_r[S], colb_r[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -154,7 +165,9 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
         const bool active = i < E.i1;
         const int64_t *nrow = E.nn + (active ? (i - E.nn_row0) : 0) * E.mp1;
 
-        // ---- gather: local index a <-> neighbor column CAP-1-a (observation last) ----
+        // ---- gather: local index a <-> neighbor column CAP-1-a (observation last).  Padding rows
+        //      get distinct far-away coordinates: their pair terms underflow to ~1e-300 (no selects
+        //      in the pair loop), their diagonal is 1 and their data 0. ----
         double rhs[1 + P][S];
         int nlive = 0;
 #pragma unroll
@@ -164,10 +177,11 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
             if (active && col < E.mp1)
                 idx = nrow[col];
             const bool live = idx >= 0;
-            double cx[D];
+            double cx[DP];
 #pragma unroll
-            for (int l = 0; l < D; ++l)
+            for (int l = 0; l < DP; ++l)
                 cx[l] = 0.0;
+            cx[0] = 1e30 * (double)(a + 1);
             rhs[0][s] = 0.0;
 #pragma unroll
             for (int b = 0; b < P; ++b)
@@ -183,28 +197,45 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
                     rhs[1 + b][s] = r[D + 1 + b];
             }
 #pragma unroll
-            for (int l = 0; l < D; ++l)
-                pts[a * D + l] = cx[l];
+            for (int l = 0; l < DP; l += 2)
+                *reinterpret_cast<double2 *>(pts + a * DP + l) = make_double2(cx[l], cx[l + 1]);
+            KLs[tri_r[s] + a] = live ? E.diag : 1.0;
             const unsigned bal = __ballot_sync(FULLMASK, live);
             nlive += __popc((G == 32) ? bal : ((bal >> (g * G)) & ((1u << (G & 31)) - 1u)));
         }
         const int pad = CAP - nlive; // identity rows at the front of the local frame
         __syncwarp();
 
-        // ---- pair terms, balanced over the lanes of the group, staged in the packed triangle ----
-        for (int t = lg; t < TRI; t += G) {
-            const unsigned ac = tab[t];
-            const int a = ac >> 8, c = ac & 255;
-            double dl[D], Kv, Dv[QD];
+        // ---- pair terms: off-diagonal pairs dealt round-robin to the lanes of the group, two
+        //      independent pairs per iteration, staged in the packed triangles ----
+        for (int t0 = lg; t0 < SM::TPAD; t0 += 2 * G) {
+            unsigned ent[2];
+            ent[0] = E.pair_tab[t0];
+            ent[1] = E.pair_tab[t0 + G];
+            double Kv[2], Dv[2][QD];
 #pragma unroll
-            for (int l = 0; l < D; ++l)
-                dl[l] = pts[a * D + l] - pts[c * D + l];
-            pair_terms_s<FAM, D>(E, dl, Kv, Dv);
-            const bool diag = (a == c), dummy = (c < pad);
-            KLs[t] = dummy ? (diag ? 1.0 : 0.0) : (diag ? E.diag : Kv);
+            for (int h = 0; h < 2; ++h) {
+                const double *pa = pts + (ent[h] >> 24) * DP;
+                const double *pc = pts + ((ent[h] >> 16) & 255) * DP;
+                double dl[D];
 #pragma unroll
-            for (int j = 0; j < QD; ++j)
-                Dms[j * TRIP + t] = (dummy || diag) ? 0.0 : Dv[j];
+                for (int l = 0; l < DP; l += 2) {
+                    const double2 va = *reinterpret_cast<const double2 *>(pa + l);
+                    const double2 vc = *reinterpret_cast<const double2 *>(pc + l);
+                    dl[l] = va.x - vc.x;
+                    if (l + 1 < D)
+                        dl[l + 1 < D ? l + 1 : l] = va.y - vc.y;
+                }
+                pair_terms_s<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kidx = ent[h] & 0xffff;
+                KLs[kidx] = Kv[h];
+#pragma unroll
+                for (int j = 0; j < QD; ++j)
+                    Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
+            }
         }
         __syncwarp();
 
@@ -232,7 +263,7 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
             failpiv = (failpiv == 0 && pv <= 0.0) ? (j + 1) : failpiv;
             if (j == CAP - 1)
                 pv_last = pv;
-            const double inv = rsqrt(pv);
+            const double inv = rsqrt_pos(pv);
             // Lo[s] = L[row][j] for rows below the pivot row, exactly 0 for finished rows, so the
             // updates below need no per-row predicates (a finished row just adds -0 * x)
             double Lo[S];
@@ -317,13 +348,14 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
 #pragma unroll 4
         for (int c = 0; c < CAP; ++c) {
             const double uc = uvec[c];
-            const int tc = c * (c + 1) / 2;
+            const int tc = c * (c - 1) / 2; // strict-lower packing: (a, c), a > c, at a(a-1)/2 + c
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                const int addr = (c < rowi[s]) ? (tri_r[s] + c) : (tc + rowi[s]);
+                const int a = rowi[s];
+                const int addr = (c < a) ? (tri_r[s] - a + c) : ((c > a) ? (tc + a) : DZERO);
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
-                    rr[r][s] = fma(Dms[r * TRIP + addr], uc, rr[r][s]);
+                    rr[r][s] = fma(Dms[r * DSZ + addr], uc, rr[r][s]);
             }
         }
 #pragma unroll
@@ -413,14 +445,18 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
         }
         const double logdet = log(pv_last);
         const bool emit = active && failpiv == 0;
+        // every lane evaluates every term (they are a handful of flops each) and keeps the ones it
+        // owns (o mod G == lane); selects instead of L divergent branches
 #pragma unroll
         for (int o = 0; o < L; ++o) {
-            if (lg == (o % G)) {
-                const double v = emit_value(o, P, Q, A, logdet, ze, we, ce, zc, wc, cc);
-                acc[o / G] += emit ? v : 0.0;
-                if (E.rows != nullptr && emit)
-                    E.rows[(size_t)(i - E.i0) * L + o] = v;
-            }
+            const double v = emit_value(o, P, Q, A, logdet, ze, we, ce, zc, wc, cc);
+            acc[o / G] += (emit && lg == (o % G)) ? v : 0.0;
+        }
+        if (E.rows != nullptr && emit) {
+#pragma unroll
+            for (int o = 0; o < L; ++o)
+                if (lg == (o % G))
+                    E.rows[(size_t)(i - E.i0) * L + o] = emit_value(o, P, Q, A, logdet, ze, we, ce, zc, wc, cc);
         }
         if (active && failpiv != 0 && lg == 0) {
             report_failure(E, i, failpiv - pad);
@@ -447,7 +483,7 @@ __global__ void __launch_bounds__(32) vecchia_tiled_kernel(const EvalParams E)
 // host side: instance table and launch
 // ---------------------------------------------------------------------------
 struct TiledInstance {
-    int g, cap, family, d, p;
+    int g, s, cap, family, d, p;
     void (*kernel)(const EvalParams);
     int smem_doubles;
     const char *name;
@@ -455,7 +491,7 @@ struct TiledInstance {
 
 #define TILED_INST(G_, S_, FAM_, D_, P_)                                                                        \
     {                                                                                                           \
-        G_, (G_) * (S_), FAM_, D_, P_, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
             TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
             "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                            \
     }
@@ -474,6 +510,45 @@ static inline const TiledInstance *tiled_find(int family, int mp1, int p, int d)
 static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
 {
     return tiled_find(family, mp1, p, d) != nullptr;
+}
+
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+// Off-diagonal pair table of a tier, built once per (device, G, S) and kept for the process
+// lifetime: entry t = a << 24 | c << 16 | (a(a+1)/2 + c) for the t-th pair (a > c) in row-major
+// order, padded to a multiple of 2G with copies of the last pair.
+static const unsigned int *tiled_pair_table(int G, int S)
+{
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, unsigned int *> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess)
+        return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple(dev, G, S);
+    auto it = cache.find(key);
+    if (it != cache.end())
+        return it->second;
+    const int cap = G * S, toff = cap * (cap - 1) / 2, tpad = (toff + 2 * G - 1) / (2 * G) * (2 * G);
+    std::vector<unsigned int> host((size_t)tpad);
+    int t = 0;
+    for (int a = 1; a < cap; ++a)
+        for (int c = 0; c < a; ++c)
+            host[t++] = ((unsigned)a << 24) | ((unsigned)c << 16) | (unsigned)(a * (a + 1) / 2 + c);
+    for (; t < tpad; ++t)
+        host[t] = host[toff - 1];
+    unsigned int *dptr = nullptr;
+    if (cudaMalloc(&dptr, sizeof(unsigned int) * tpad) != cudaSuccess)
+        return nullptr;
+    if (cudaMemcpy(dptr, host.data(), sizeof(unsigned int) * tpad, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(dptr);
+        return nullptr;
+    }
+    cache[key] = dptr;
+    return dptr;
 }
 
 // returns 0, -100 (CUDA error pending), or a VB200_E* code
@@ -505,6 +580,10 @@ static int launch_tiled(cudaStream_t stream, int sm_count, size_t smem_optin, Ev
     if (!partials)
         return -3;
     E.partials = partials;
+    E.pair_tab = tiled_pair_table(t->g, t->s);
+    if (!E.pair_tab)
+        return -100;
+    cudaFuncSetAttribute(t->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     t->kernel<<<(unsigned)blocks, 32, smem, stream>>>(E);
     if (cudaGetLastError() != cudaSuccess)
         return -100;
