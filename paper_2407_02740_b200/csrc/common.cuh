@@ -26,6 +26,7 @@ struct EvalParams {
     int L;                  // accumulator length
     double sig2, tau2, jitter, diag; // diag = sig2*(1+tau2) + jitter
     double inv_sig2;
+    double piv_floor;       // a pivot <= piv_floor fails the factorization (see vecchia_b200.cu fill_params)
     double inv_rho[VB_MAXD]; // per-axis inverse ranges (iso: all equal; space-time: space,..,space,time)
     double *partials;        // [gridDim.x][L] block partial sums
     unsigned long long *fail_word; // min over failures of (index << 16 | pivot+1)
@@ -73,7 +74,9 @@ __device__ __forceinline__ double sqrt_pos(double a)
 // error 2.2e-16 against libm on [0, 50]; x is clamped at 700 (result ~1e-304, never denormal).
 __device__ __forceinline__ double exp_neg(double x, const double *tab)
 {
-    x = fmin(x, 700.0);
+    // clamp at ~700 with one integer min on the high word (x >= 0, so the IEEE order is the
+    // integer order; the low word of a clamped value is irrelevant)
+    x = __hiloint2double(min(__double2hiint(x), 0x4085e000), __double2loint(x));
     const double kf = fma(x, -92.33248261689366, 6755399441055744.0);
     const int ki = __double2loint(kf);
     const double kd = kf - 6755399441055744.0;

@@ -32,22 +32,23 @@ struct FamTraits {
     static constexpr int Q = QD + 2;
 };
 
-// pair terms with a compile-time coordinate count (registers only, no local arrays)
+// Pair terms with a compile-time coordinate count.  dl[] are coordinate differences ALREADY
+// divided by the range of their axis (the gather scales the coordinates once per point), so the
+// squared norm is x^2 = (r/rho)^2 directly.  Squared norms start from 1e-300 instead of 0:
+// coincident points then give x ~ 1e-150, i.e. exactly the reference's values (exp(-0) = 1, zero
+// range derivative) without a special case.
 template <int FAM, int D>
 __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *etab, const double (&dl)[D],
                                              double &Kv, double (&Dv)[FamTraits<FAM, D>::QD])
 {
-    // squared distances start from 1e-300 instead of 0: coincident points then give x ~ 1e-150,
-    // i.e. exactly the reference's values (exp(-0) = 1, zero range derivative) with no special case
     if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
-        double d2 = 1e-300;
+        double x2 = 1e-300;
 #pragma unroll
         for (int l = 0; l < D; ++l)
-            d2 = fma(dl[l], dl[l], d2);
-        const double ir = E.inv_rho[0];
-        const double x = sqrt_pos(d2) * ir;
+            x2 = fma(dl[l], dl[l], x2);
+        const double x = x2 * rsqrt_pos(x2);
         const double se = E.sig2 * exp_neg(x, etab);
-        const double xi = x * ir;
+        const double xi = x * E.inv_rho[0];
         if constexpr (FAM == FAM_EXP_ISO) {
             Kv = se;
             Dv[0] = se * xi;
@@ -64,15 +65,13 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
         double s2 = 1e-300, sp2 = 0.0;
 #pragma unroll
         for (int l = 0; l < D; ++l) {
-            const double t = dl[l] * E.inv_rho[l];
-            sc[l] = t * t;
+            sc[l] = dl[l] * dl[l];
             s2 += sc[l];
             if (l < D - 1)
                 sp2 += sc[l];
         }
         const double rs = rsqrt_pos(s2);
-        const double s = s2 * rs;
-        Kv = E.sig2 * exp_neg(s, etab);
+        Kv = E.sig2 * exp_neg(s2 * rs, etab);
         const double g = Kv * rs;
         if constexpr (FAM == FAM_EXP_ANISO) {
 #pragma unroll
@@ -108,9 +107,10 @@ struct TileSmem {
     static constexpr int DSZ = (DOFF + 1 + 1) & ~1;         // + one zero slot (the diagonal of D_j)
     static constexpr int PER_OBS = PTS + Geo::KL + QD * DSZ;
     static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
+    // Local row 0 is ALWAYS a padding row (tiers serve m+1 <= CAP-1), so nothing is computed for it.
     // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
     // multiple of 2G with copies of the last pair; entry = a << 24 | c << 16 | packed index tri(a)+c
-    static constexpr int TOFF = DOFF;
+    static constexpr int TOFF = (Geo::CAP - 1) * (Geo::CAP - 2) / 2; // pairs among local rows 1..CAP-1
     static constexpr int TPAD = (TOFF + 2 * G - 1) / (2 * G) * (2 * G);
 };
 
@@ -142,10 +142,14 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
 
     for (int t = lane; t < VB_EXPTAB; t += 32)
         etab[t] = exp2((double)t * (1.0 / VB_EXPTAB));
-    if (lg == 0)
+    // zero slot (diagonal of D_j) and column 0 of D_j (padding row, never written by the pair loop)
 #pragma unroll
-        for (int j = 0; j < QD; ++j)
+    for (int j = 0; j < QD; ++j) {
+        if (lg == 0)
             Dms[j * DSZ + DZERO] = 0.0;
+        for (int a = 1 + lg; a < CAP; a += G)
+            Dms[j * DSZ + a * (a - 1) / 2] = 0.0;
+    }
     int rowi[S], tri_r[S], colb_r[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -165,9 +169,8 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         const bool active = i < E.i1;
         const int64_t *nrow = E.nn + (active ? (i - E.nn_row0) : 0) * E.mp1;
 
-        // ---- gather: local index a <-> neighbor column CAP-1-a (observation last).  Padding rows
-        //      get distinct far-away coordinates: their pair terms underflow to ~1e-300 (no selects
-        //      in the pair loop), their diagonal is 1 and their data 0. ----
+        // ---- gather: local index a <-> neighbor column CAP-1-a (observation last).  Coordinates are
+        //      stored divided by the range of their axis.  Padding rows: diagonal 1, data 0. ----
         double rhs[1 + P][S];
         int nlive = 0;
 #pragma unroll
@@ -181,7 +184,6 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
 #pragma unroll
             for (int l = 0; l < DP; ++l)
                 cx[l] = 0.0;
-            cx[0] = 1e30 * (double)(a + 1);
             rhs[0][s] = 0.0;
 #pragma unroll
             for (int b = 0; b < P; ++b)
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                 const double *r = E.rec + idx * E.rs;
 #pragma unroll
                 for (int l = 0; l < D; ++l)
-                    cx[l] = r[l];
+                    cx[l] = r[l] * E.inv_rho[l];
                 rhs[0][s] = r[D];
 #pragma unroll
                 for (int b = 0; b < P; ++b)
@@ -206,35 +208,56 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         const int pad = CAP - nlive; // identity rows at the front of the local frame
         __syncwarp();
 
-        // ---- pair terms: off-diagonal pairs dealt round-robin to the lanes of the group, two
-        //      independent pairs per iteration, staged in the packed triangles ----
-        for (int t0 = lg; t0 < SM::TPAD; t0 += 2 * G) {
-            unsigned ent[2];
-            ent[0] = E.pair_tab[t0];
-            ent[1] = E.pair_tab[t0 + G];
-            double Kv[2], Dv[2][QD];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const double *pa = pts + (ent[h] >> 24) * DP;
-                const double *pc = pts + ((ent[h] >> 16) & 255) * DP;
-                double dl[D];
-#pragma unroll
-                for (int l = 0; l < DP; l += 2) {
-                    const double2 va = *reinterpret_cast<const double2 *>(pa + l);
-                    const double2 vc = *reinterpret_cast<const double2 *>(pc + l);
-                    dl[l] = va.x - vc.x;
-                    if (l + 1 < D)
-                        dl[l + 1 < D ? l + 1 : l] = va.y - vc.y;
+        // ---- pair terms.  The table lists the off-diagonal pairs (a > c) by DESCENDING c, so the
+        //      k(k-1)/2 pairs of the live points come first; they are dealt round-robin to the lanes
+        //      of the group, two independent pairs per iteration (ILP), and staged in the packed
+        //      triangles.  Pairs that touch a padding row are just zero-filled. ----
+        const int nlp = nlive * (nlive - 1) / 2;
+        {
+            unsigned ent[2], nxt[2];
+            nxt[0] = E.pair_tab[lg];
+            nxt[1] = E.pair_tab[lg + G];
+            for (int t0 = lg; t0 < nlp; t0 += 2 * G) {
+                ent[0] = nxt[0];
+                ent[1] = nxt[1];
+                if (t0 + 2 * G < SM::TPAD) { // prefetch the next pair of entries (L1-resident table)
+                    nxt[0] = E.pair_tab[t0 + 2 * G];
+                    nxt[1] = E.pair_tab[t0 + 3 * G];
                 }
-                pair_terms_s<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
-            }
+                double Kv[2], Dv[2][QD];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int kidx = ent[h] & 0xffff;
-                KLs[kidx] = Kv[h];
+                for (int h = 0; h < 2; ++h) {
+                    const double *pa = pts + (ent[h] >> 24) * DP;
+                    const double *pc = pts + ((ent[h] >> 16) & 255) * DP;
+                    double dl[D];
+#pragma unroll
+                    for (int l = 0; l < DP; l += 2) {
+                        const double2 va = *reinterpret_cast<const double2 *>(pa + l);
+                        const double2 vc = *reinterpret_cast<const double2 *>(pc + l);
+                        dl[l] = va.x - vc.x;
+                        if (l + 1 < D)
+                            dl[l + 1 < D ? l + 1 : l] = va.y - vc.y;
+                    }
+                    pair_terms_s<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (t0 + h * G < nlp) {
+                        const int kidx = ent[h] & 0xffff;
+                        KLs[kidx] = Kv[h];
+#pragma unroll
+                        for (int j = 0; j < QD; ++j)
+                            Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
+                    }
+                }
+            }
+            for (int t = nlp + lg; t < SM::TOFF; t += G) {
+                const unsigned e0 = E.pair_tab[t];
+                const int kidx = e0 & 0xffff;
+                KLs[kidx] = 0.0;
 #pragma unroll
                 for (int j = 0; j < QD; ++j)
-                    Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
+                    Dms[j * DSZ + kidx - (int)(e0 >> 24)] = 0.0;
             }
         }
         __syncwarp();
@@ -252,15 +275,15 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         double invd[S];
 #pragma unroll
         for (int s = 0; s < S; ++s)
-            invd[s] = 0.0;
+            invd[s] = 1.0;
         int failpiv = 0;
         double pv_last = 1.0;
 #pragma unroll
-        for (int j = 0; j < CAP; ++j) {
+        for (int j = 1; j < CAP; ++j) { // local row 0 is always padding: step 0 is the identity
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
             const double pv = __shfl_sync(FULLMASK, Kr[sj][j], oj, G);
-            failpiv = (failpiv == 0 && pv <= 0.0) ? (j + 1) : failpiv;
+            failpiv = (failpiv == 0 && pv <= E.piv_floor) ? (j + 1) : failpiv;
             if (j == CAP - 1)
                 pv_last = pv;
             const double inv = rsqrt_pos(pv);
@@ -319,7 +342,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         for (int s = 0; s < S; ++s)
             ub[s] = (rowi[s] == CAP - 1) ? 1.0 : 0.0;
 #pragma unroll
-        for (int l = CAP - 1; l >= 0; --l) {
+        for (int l = CAP - 1; l >= 1; --l) {
             const int sl = l / G;
             const int ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
             const double ul = __shfl_sync(FULLMASK, ub[sl] * invd[sl], ol, G);
@@ -333,7 +356,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         }
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            ub[s] *= invd[s];
+            ub[s] = (rowi[s] < pad) ? 0.0 : ub[s] * invd[s]; // padding rows: u = 0 whatever was read
             uvec[rowi[s]] = ub[s];
         }
         __syncwarp();
@@ -346,7 +369,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
             for (int s = 0; s < S; ++s)
                 rr[r][s] = 0.0;
 #pragma unroll 4
-        for (int c = 0; c < CAP; ++c) {
+        for (int c = 1; c < CAP; ++c) {
             const double uc = uvec[c];
             const int tc = c * (c - 1) / 2; // strict-lower packing: (a, c), a > c, at a(a-1)/2 + c
 #pragma unroll
@@ -362,7 +385,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         for (int s = 0; s < S; ++s)
             rr[QD][s] = ub[s];
 #pragma unroll
-        for (int j = 0; j < CAP; ++j) {
+        for (int j = 1; j < CAP; ++j) {
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
             double Lm[S];
@@ -502,7 +525,7 @@ static inline const TiledInstance *tiled_find(int family, int mp1, int p, int d)
 {
     const TiledInstance *best = nullptr;
     for (const TiledInstance &t : kTiledInstances)
-        if (t.family == family && t.d == d && t.p == p && t.cap >= mp1 && (!best || t.cap < best->cap))
+        if (t.family == family && t.d == d && t.p == p && t.cap - 1 >= mp1 && (!best || t.cap < best->cap))
             best = &t;
     return best;
 }
@@ -518,8 +541,9 @@ static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
 #include <vector>
 
 // Off-diagonal pair table of a tier, built once per (device, G, S) and kept for the process
-// lifetime: entry t = a << 24 | c << 16 | (a(a+1)/2 + c) for the t-th pair (a > c) in row-major
-// order, padded to a multiple of 2G with copies of the last pair.
+// lifetime: entry t = a << 24 | c << 16 | (a(a+1)/2 + c) for the t-th pair (a > c), pairs ordered
+// by descending c (so the pairs among the LAST k local points are the first k(k-1)/2 entries),
+// padded to a multiple of 2G with copies of the last pair.
 static const unsigned int *tiled_pair_table(int G, int S)
 {
     static std::mutex mu;
@@ -532,11 +556,11 @@ static const unsigned int *tiled_pair_table(int G, int S)
     auto it = cache.find(key);
     if (it != cache.end())
         return it->second;
-    const int cap = G * S, toff = cap * (cap - 1) / 2, tpad = (toff + 2 * G - 1) / (2 * G) * (2 * G);
+    const int cap = G * S, toff = (cap - 1) * (cap - 2) / 2, tpad = (toff + 2 * G - 1) / (2 * G) * (2 * G);
     std::vector<unsigned int> host((size_t)tpad);
     int t = 0;
-    for (int a = 1; a < cap; ++a)
-        for (int c = 0; c < a; ++c)
+    for (int c = cap - 2; c >= 1; --c) // descending c: the pairs among the last k points come first
+        for (int a = c + 1; a < cap; ++a)
             host[t++] = ((unsigned)a << 24) | ((unsigned)c << 16) | (unsigned)(a * (a + 1) / 2 + c);
     for (; t < tpad; ++t)
         host[t] = host[toff - 1];

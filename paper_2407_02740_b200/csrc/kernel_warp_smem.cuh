@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(WS_WARPS_MAX * 32) vecchia_warp_smem_kernel(co
         int failed = 0;
         for (int j = 0; j < k; ++j) {
             const double piv = Km[j * ld + j];
-            if (piv <= 0.0) {
+            if (piv <= P.piv_floor) {
                 failed = j + 1;
                 break;
             }

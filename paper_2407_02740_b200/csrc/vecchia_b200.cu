@@ -375,6 +375,12 @@ static int fill_params(const vb200_problem *P, int family, const double *theta, 
     E.jitter = jitter;
     E.diag = theta[0] * (1.0 + theta[q - 1]) + jitter;
     E.inv_sig2 = 1.0 / theta[0];
+    // The reference fails a factorization when a pivot is <= 0 (_kernels.pyx:246-249).  For an
+    // exactly singular local matrix (duplicated location, zero nugget) that pivot is pure rounding
+    // residue, +-1e-16 * diag, whose sign depends on the summation order; the reference's order
+    // happens to give <= 0 (pinned by its tests/test_engine.py:230-243).  To report the same
+    // failures independently of summation order, a pivot within 1e-14 * diag of zero also fails.
+    E.piv_floor = 1e-14 * E.diag;
     for (int l = 0; l < P->d; ++l) {
         double rho;
         if (family == VB200_EXP_ANISO)
