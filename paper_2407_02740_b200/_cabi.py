@@ -58,7 +58,9 @@ def load(build_if_missing: bool = True):
     if _lib is None:
         from . import build
         try:
-            path = build.build_cuda() if build_if_missing else build.CUDA_LIB
+            import os
+            override = os.environ.get("VB200_LIB")  # development: load an alternative build of the same ABI
+            path = override or (build.build_cuda() if build_if_missing else build.CUDA_LIB)
             lib = ctypes.CDLL(str(path))
         except (OSError, RuntimeError, Exception) as err:  # noqa: BLE001 - anything here means "no CUDA core"
             raise DeviceUnavailable(f"cannot load the CUDA core ({err}); there is no CPU fallback") from err

@@ -58,6 +58,15 @@ __device__ __forceinline__ double rsqrt_pos(double a)
     return fma(t, y * e, y);
 }
 
+// 1/a for positive normal a: MUFU.RCP64H seed + two Newton steps
+__device__ __forceinline__ double rcp_pos(double a)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    r = fma(fma(-a, r, 1.0), r, r);
+    return fma(fma(-a, r, 1.0), r, r);
+}
+
 // sqrt(a): a * rsqrt(a) with one Newton correction of the product (correctly rounded in practice)
 __device__ __forceinline__ double sqrt_pos(double a)
 {

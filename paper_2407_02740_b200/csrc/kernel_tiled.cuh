@@ -25,6 +25,9 @@
 #include "common.cuh"
 
 #define FULLMASK 0xffffffffu
+#ifndef TILED_NI
+#define TILED_NI 2 // independent pairs in flight per lane in the pair loop (3 and 4 measured no faster)
+#endif
 
 template <int FAM, int D>
 struct FamTraits {
@@ -89,11 +92,11 @@ struct TileGeom {
     static constexpr int CAP = G * S;
     static constexpr int OPW = 32 / G;                 // observations per warp
     static constexpr int TRI = CAP * (CAP + 1) / 2;    // packed lower triangle incl. diagonal
-    // column store of L: element (c, j), c >= j, lives at colbase(j) + c; colbase(j) is even so
-    // that pairs (c, c+1) with c even are 16-byte aligned (CAP is even for every tier)
-    __host__ __device__ static constexpr int colbase(int j) { return j * (CAP - 1) - j * (j - 1) / 2 + (j + 1) / 2; }
-    static constexpr int LST = colbase(CAP - 1) + CAP; // doubles in the column store
-    static constexpr int KL = ((LST > TRI ? LST : TRI) + 1) & ~1;
+    // column store: element (c, j), c >= j, of the (unscaled) factor lives at colbase(j) + c, columns
+    // packed back to back.  colbase(j) = -j(j+1)/2 (mod 16) when CAP = 32, so the 16 lanes of a group
+    // reading "their" columns at a common row hit 16 different 8-byte banks.
+    __host__ __device__ static constexpr int colbase(int j) { return j * (CAP - 1) - j * (j - 1) / 2; }
+    static constexpr int KL = TRI + 2; // one element past the last column may be read by a pair load
     __host__ __device__ static constexpr int slot_of(int r) { return r / G; }
     __host__ __device__ static constexpr int lane_of(int r) { return ((r / G) & 1) ? (G - 1 - r % G) : (r % G); }
 };
@@ -109,13 +112,16 @@ struct TileSmem {
     static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
     // Local row 0 is ALWAYS a padding row (tiers serve m+1 <= CAP-1), so nothing is computed for it.
     // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
-    // multiple of 2G with copies of the last pair; entry = a << 24 | c << 16 | packed index tri(a)+c
+    // multiple of NI*G with copies of the last pair; entry = a << 24 | c << 16 | packed index tri(a)+c
     static constexpr int TOFF = (Geo::CAP - 1) * (Geo::CAP - 2) / 2; // pairs among local rows 1..CAP-1
-    static constexpr int TPAD = (TOFF + 2 * G - 1) / (2 * G) * (2 * G);
+    static constexpr int NI = TILED_NI;                            // pairs in flight per lane in the pair loop
+    static constexpr int TPAD = (TOFF + NI * G - 1) / (NI * G) * (NI * G);
 };
 
 // blocks per SM the register budget is tuned for (one warp per block): 3 warps per SM sub-partition
+#ifndef TILED_MIN_BLOCKS
 #define TILED_MIN_BLOCKS 12
+#endif
 
 template <int G, int S, int FAM, int D, int P>
 __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(const EvalParams E)
@@ -135,8 +141,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
     const int lane = threadIdx.x;
     const int g = lane / G, lg = lane % G;
     double *obs = smem + VB_EXPTAB + g * SM::PER_OBS;
-    double *pts = obs;                               // CAP x DP coordinates of the local frame ...
-    double *uvec = obs;                              // ... later u = B^-T e_last (coordinates are dead by then)
+    double *pts = obs;                               // CAP x DP scaled coordinates of the local frame
     double *KLs = obs + SM::PTS;                     // packed K staging, then the column store of L
     double *Dms = KLs + Geo::KL;                     // QD packed strict-lower derivative matrices (+ zero slot)
 
@@ -214,19 +219,24 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         //      triangles.  Pairs that touch a padding row are just zero-filled. ----
         const int nlp = nlive * (nlive - 1) / 2;
         {
-            unsigned ent[2], nxt[2];
-            nxt[0] = E.pair_tab[lg];
-            nxt[1] = E.pair_tab[lg + G];
-            for (int t0 = lg; t0 < nlp; t0 += 2 * G) {
-                ent[0] = nxt[0];
-                ent[1] = nxt[1];
-                if (t0 + 2 * G < SM::TPAD) { // prefetch the next pair of entries (L1-resident table)
-                    nxt[0] = E.pair_tab[t0 + 2 * G];
-                    nxt[1] = E.pair_tab[t0 + 3 * G];
-                }
-                double Kv[2], Dv[2][QD];
+            constexpr int NI = SM::NI; // independent pairs in flight per lane (ILP; registers are free here)
+            unsigned nxt[NI];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NI; ++h)
+                nxt[h] = E.pair_tab[lg + h * G];
+            for (int t0 = lg; t0 < nlp; t0 += NI * G) {
+                unsigned ent[NI];
+#pragma unroll
+                for (int h = 0; h < NI; ++h)
+                    ent[h] = nxt[h];
+                if (t0 + NI * G < SM::TPAD) { // prefetch the next entries (L1-resident table)
+#pragma unroll
+                    for (int h = 0; h < NI; ++h)
+                        nxt[h] = E.pair_tab[t0 + (NI + h) * G];
+                }
+                double Kv[NI], Dv[NI][QD];
+#pragma unroll
+                for (int h = 0; h < NI; ++h) {
                     const double *pa = pts + (ent[h] >> 24) * DP;
                     const double *pc = pts + ((ent[h] >> 16) & 255) * DP;
                     double dl[D];
@@ -240,17 +250,18 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                     }
                     pair_terms_s<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
                 }
+                // entries past nlp in the last iteration belong to padding pairs: they are written
+                // here and overwritten with zeros below (after the warp sync)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (t0 + h * G < nlp) {
-                        const int kidx = ent[h] & 0xffff;
-                        KLs[kidx] = Kv[h];
+                for (int h = 0; h < NI; ++h) {
+                    const int kidx = ent[h] & 0xffff;
+                    KLs[kidx] = Kv[h];
 #pragma unroll
-                        for (int j = 0; j < QD; ++j)
-                            Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
-                    }
+                    for (int j = 0; j < QD; ++j)
+                        Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
                 }
             }
+            __syncwarp();
             for (int t = nlp + lg; t < SM::TOFF; t += G) {
                 const unsigned e0 = E.pair_tab[t];
                 const int kidx = e0 & 0xffff;
@@ -271,121 +282,131 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                 Kr[s][c] = KLs[tri_r[s] + c];
         __syncwarp();
 
-        // ---- Cholesky (right-looking) with the forward substitutions of y and X fused in ----
-        double invd[S];
+        // ---- square-root-free factorization K = Lt D Lt^T (Lt unit lower, D = diag(d)), right-looking,
+        //      with the forward substitutions of y and X fused in.  The Cholesky factor of the reference
+        //      is B = Lt D^(1/2); working with Lt and d keeps sqrt AND the diagonal scalings out of every
+        //      dependent chain: at step j the UNSCALED column j (d_j on top) goes to the column store
+        //      as soon as the previous update is done, and 1/d_j is formed by all lanes from the
+        //      broadcast read, in parallel with the rest of the column loads. ----
+        double invd[S]; // 1/d_a of the own rows
 #pragma unroll
         for (int s = 0; s < S; ++s)
             invd[s] = 1.0;
         int failpiv = 0;
-        double pv_last = 1.0;
 #pragma unroll
-        for (int j = 1; j < CAP; ++j) { // local row 0 is always padding: step 0 is the identity
+        for (int j = 1; j < CAP - 1; ++j) { // local row 0 is always padding: step 0 is the identity
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
-            const double pv = __shfl_sync(FULLMASK, Kr[sj][j], oj, G);
-            failpiv = (failpiv == 0 && pv <= E.piv_floor) ? (j + 1) : failpiv;
-            if (j == CAP - 1)
-                pv_last = pv;
-            const double inv = rsqrt_pos(pv);
-            // Lo[s] = L[row][j] for rows below the pivot row, exactly 0 for finished rows, so the
-            // updates below need no per-row predicates (a finished row just adds -0 * x)
+            const double *col = KLs + Geo::colbase(j);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if ((s + 1) * G - 1 >= j && rowi[s] >= j)
+                    KLs[Geo::colbase(j) + rowi[s]] = Kr[s][j];
+            double xr[1 + P];
+#pragma unroll
+            for (int r = 0; r < 1 + P; ++r)
+                xr[r] = __shfl_sync(FULLMASK, rhs[r][sj], oj, G); // (Lt^-1 rhs)_j is final at step j
+            __syncwarp();
+            // pairs (c0, c0+1) are read as one 128-bit broadcast load; the parity of the first pair is
+            // static (colbase(j) + c0 must be even)
+            const int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
+            double dj;
+            if (cs != j)
+                dj = col[j];
+            double2 v0;
+            if (cs == j) {
+                v0 = *reinterpret_cast<const double2 *>(col + j);
+                dj = v0.x;
+            }
+            failpiv = (failpiv == 0 && dj <= E.piv_floor) ? (j + 1) : failpiv;
+            const double rj = rcp_pos(dj);
+            // Lo[s] = Lt[row][j] for rows below the pivot row, exactly 0 for finished rows, so the
+            // updates need no per-row predicates (a finished row just adds -0 * x)
             double Lo[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if ((s + 1) * G - 1 >= j) { // slot still has rows >= j
-                    const double Lraw = Kr[s][j] * inv;
-                    Kr[s][j] = Lraw;
-                    Lo[s] = (rowi[s] > j) ? Lraw : 0.0;
-                    if (rowi[s] > j)
-                        KLs[Geo::colbase(j) + rowi[s]] = Lraw;
-                    invd[s] = (rowi[s] == j) ? inv : invd[s];
+                if ((s + 1) * G - 1 > j) {
+                    const double Ls = Kr[s][j] * rj;
+                    Lo[s] = (rowi[s] > j) ? Ls : 0.0;
+                    Kr[s][j] = Ls;
                 } else {
                     Lo[s] = 0.0;
                 }
+                if ((s + 1) * G - 1 >= j)
+                    invd[s] = (rowi[s] == j) ? rj : invd[s];
             }
-            // forward substitution of y and X rides along; the pivot row keeps its unscaled
-            // value (z_j = rhs_j * invd_j is applied once after the sweep)
 #pragma unroll
-            for (int r = 0; r < 1 + P; ++r) {
-                const double xr = __shfl_sync(FULLMASK, rhs[r][sj], oj, G) * inv;
+            for (int r = 0; r < 1 + P; ++r)
 #pragma unroll
                 for (int s = 0; s < S; ++s)
                     if ((s + 1) * G - 1 > j)
-                        rhs[r][s] = fma(-Lo[s], xr, rhs[r][s]);
+                        rhs[r][s] = fma(-Lo[s], xr[r], rhs[r][s]);
+            if (cs == j) {
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if ((s + 1) * G - 1 >= j + 1)
+                        Kr[s][j + 1] = fma(-Lo[s], v0.y, Kr[s][j + 1]);
             }
-            __syncwarp();
-            if (j + 1 < CAP) {
-                const double *col = KLs + Geo::colbase(j);
 #pragma unroll
-                for (int c0 = (j + 1) & ~1; c0 < CAP; c0 += 2) {
-                    const double2 v = *reinterpret_cast<const double2 *>(col + c0);
+            for (int c0 = (cs == j) ? j + 2 : j + 1; c0 < CAP; c0 += 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(col + c0);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        if (c0 > j && (s + 1) * G - 1 >= c0)
-                            Kr[s][c0] = fma(-Lo[s], v.x, Kr[s][c0]);
-                        if ((s + 1) * G - 1 >= c0 + 1)
-                            Kr[s][c0 + 1] = fma(-Lo[s], v.y, Kr[s][c0 + 1]);
-                    }
+                for (int s = 0; s < S; ++s) {
+                    if ((s + 1) * G - 1 >= c0)
+                        Kr[s][c0] = fma(-Lo[s], v.x, Kr[s][c0]);
+                    if (c0 + 1 < CAP && (s + 1) * G - 1 >= c0 + 1)
+                        Kr[s][c0 + 1] = fma(-Lo[s], v.y, Kr[s][c0 + 1]);
                 }
             }
         }
+        // last pivot d_e (row CAP-1 = the observation itself): nothing left to update
+        constexpr int se = S - 1;
+        constexpr int oe = Geo::lane_of(CAP - 1);
+        const double d_e = __shfl_sync(FULLMASK, Kr[se][CAP - 1], oe, G);
+        failpiv = (failpiv == 0 && d_e <= E.piv_floor) ? CAP : failpiv;
+        const double rho_e = rcp_pos(d_e);
+        invd[se] = (rowi[se] == CAP - 1) ? rho_e : invd[se];
 
+        // ---- ut = Lt^-T e_last (u = ut / sqrt(d_e)): the lane owning index j accumulates
+        //      sb_j = sum_{l>j} K(l,j) ut_l from the unscaled column store, ut_j = e_j - sb_j / d_j.  As
+        //      soon as ut_l is known (and broadcast) it is also applied to the packed derivative
+        //      matrices, tt_r += D_r[., l] ut_l, so D_r u needs no separate mat-vec pass.  Element
+        //      (a, l) of the symmetric D_r lives at a(a-1)/2 + l (a > l) or l(l-1)/2 + a (a < l); for
+        //      a == l the first form points at D[a+1][0], a column-0 entry, which is always zero. ----
+        double sb[S], eb[S], rr[QD + 1][S];
 #pragma unroll
-        for (int r = 0; r < 1 + P; ++r)
+        for (int s = 0; s < S; ++s) {
+            sb[s] = 0.0;
+            eb[s] = (rowi[s] == CAP - 1) ? 1.0 : 0.0;
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-                rhs[r][s] *= invd[s];
-
-        // ---- u = B^-T e_last: lane owning index j reads column j of L from the column store ----
-        double ub[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s)
-            ub[s] = (rowi[s] == CAP - 1) ? 1.0 : 0.0;
+            for (int r = 0; r < QD; ++r)
+                rr[r][s] = 0.0;
+        }
 #pragma unroll
         for (int l = CAP - 1; l >= 1; --l) {
             const int sl = l / G;
             const int ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
-            const double ul = __shfl_sync(FULLMASK, ub[sl] * invd[sl], ol, G);
+            const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
+                const bool above = rowi[s] < l;
                 if (s * G < l) { // slot has rows < l
-                    const double Llj = (rowi[s] < l) ? KLs[colb_r[s] + l] : 0.0;
-                    ub[s] = fma(-Llj, ul, ub[s]);
+                    const double Klj = above ? KLs[colb_r[s] + l] : 0.0;
+                    sb[s] = fma(Klj, ul, sb[s]);
                 }
-            }
-        }
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            ub[s] = (rowi[s] < pad) ? 0.0 : ub[s] * invd[s]; // padding rows: u = 0 whatever was read
-            uvec[rowi[s]] = ub[s];
-        }
-        __syncwarp();
-
-        // ---- t_j = D_j u (symmetric packed mat-vec), then [t_1..t_QD, u] through B^-1 ----
-        double rr[QD + 1][S];
-#pragma unroll
-        for (int r = 0; r < QD; ++r)
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                rr[r][s] = 0.0;
-#pragma unroll 4
-        for (int c = 1; c < CAP; ++c) {
-            const double uc = uvec[c];
-            const int tc = c * (c - 1) / 2; // strict-lower packing: (a, c), a > c, at a(a-1)/2 + c
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int a = rowi[s];
-                const int addr = (c < a) ? (tri_r[s] - a + c) : ((c > a) ? (tc + a) : DZERO);
+                const int addr = above ? (l * (l - 1) / 2 + rowi[s]) : (tri_r[s] - rowi[s] + l);
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
-                    rr[r][s] = fma(Dms[r * DSZ + addr], uc, rr[r][s]);
+                    rr[r][s] = fma(Dms[r * DSZ + addr], ul, rr[r][s]);
             }
         }
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            rr[QD][s] = ub[s];
+        for (int s = 0; s < S; ++s) // padding rows: ut = 0 whatever was read
+            rr[QD][s] = (rowi[s] < pad) ? 0.0 : fma(-sb[s], invd[s], eb[s]);
+
+        // ---- [tt_1..tt_QD, ut] through Lt^-1 (unit-diagonal forward sweeps on the register-resident rows) ----
 #pragma unroll
-        for (int j = 1; j < CAP; ++j) {
+        for (int j = 1; j < CAP - 1; ++j) {
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
             double Lm[S];
@@ -394,21 +415,17 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                 Lm[s] = ((s + 1) * G - 1 > j && rowi[s] > j) ? Kr[s][j] : 0.0;
 #pragma unroll
             for (int r = 0; r < QD + 1; ++r) {
-                const double x = __shfl_sync(FULLMASK, rr[r][sj] * invd[sj], oj, G);
+                const double x = __shfl_sync(FULLMASK, rr[r][sj], oj, G);
 #pragma unroll
                 for (int s = 0; s < S; ++s)
                     if ((s + 1) * G - 1 > j)
                         rr[r][s] = fma(-Lm[s], x, rr[r][s]);
             }
         }
-#pragma unroll
-        for (int r = 0; r < QD + 1; ++r)
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                rr[r][s] *= invd[s];
-        // now rr[r] = c_dense_r (r < QD), rr[QD] = w = B^-1 u; rhs[0] = z, rhs[1+b] = W_b
-
-        // ---- dot products over the local index, reduced over the G lanes of the group ----
+        // Now, with <a,b> = sum_a a_a b_a / d_a and s = 1/sqrt(d_e):
+        //   z = D^-1/2 yt, W = D^-1/2 Xt            (yt = rhs[0], Xt = rhs[1+b])
+        //   c_r = s D^-1/2 ct_r, w = B^-1 u = s D^-1/2 wt   (ct_r = rr[r], wt = rr[QD])
+        // so every dot product below is a weighted dot of the tilde vectors times s or s^2.
         auto gsum = [](double v) {
 #pragma unroll
             for (int off = G / 2; off > 0; off >>= 1)
@@ -422,18 +439,23 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                 s0 = fma(x[s], y[s], s0);
             return gsum(s0);
         };
-        constexpr int se = S - 1;
-        constexpr int oe = Geo::lane_of(CAP - 1);
-        const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G);
-        const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G);
+        const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
+        const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
+        const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G) * rho_e;
         double we[P], ce[Q], zc[Q], wc[P * Q], cc[Q * Q];
 #pragma unroll
         for (int b = 0; b < P; ++b)
-            we[b] = __shfl_sync(FULLMASK, rhs[1 + b][se], oe, G);
+            we[b] = __shfl_sync(FULLMASK, rhs[1 + b][se], oe, G) * sq;
+        double rrw[QD + 1][S]; // ct_r / d, wt / d
+#pragma unroll
+        for (int r = 0; r < QD + 1; ++r)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                rrw[r][s] = rr[r][s] * invd[s];
         const double jit = E.jitter, is2 = E.inv_sig2, s2 = E.sig2;
         {
-            const double zw = dot(rhs[0], rr[QD]);
-            const double ww = dot(rr[QD], rr[QD]);
+            const double zw = dot(rhs[0], rrw[QD]) * sq;
+            const double ww = dot(rr[QD], rrw[QD]) * rho_e;
             ce[0] = (1.0 - jit * w_e) * is2;
             ce[Q - 1] = s2 * w_e;
             zc[0] = (ze - jit * zw) * is2;
@@ -443,30 +465,30 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
             cc[(Q - 1) * Q + Q - 1] = s2 * s2 * ww;
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                const double Ww = dot(rhs[1 + b], rr[QD]);
+                const double Ww = dot(rhs[1 + b], rrw[QD]) * sq;
                 wc[b * Q] = (we[b] - jit * Ww) * is2;
                 wc[b * Q + Q - 1] = s2 * Ww;
             }
 #pragma unroll
             for (int r = 0; r < QD; ++r) {
-                const double cde = __shfl_sync(FULLMASK, rr[r][se], oe, G);
-                const double wcd = dot(rr[QD], rr[r]);
+                const double cde = __shfl_sync(FULLMASK, rr[r][se], oe, G) * rho_e;
+                const double wcd = dot(rr[QD], rrw[r]) * rho_e;
                 ce[1 + r] = cde;
-                zc[1 + r] = dot(rhs[0], rr[r]);
+                zc[1 + r] = dot(rhs[0], rrw[r]) * sq;
                 cc[1 + r] = cc[(1 + r) * Q] = (cde - jit * wcd) * is2;
                 cc[(1 + r) * Q + Q - 1] = cc[(Q - 1) * Q + 1 + r] = s2 * wcd;
 #pragma unroll
                 for (int b = 0; b < P; ++b)
-                    wc[b * Q + 1 + r] = dot(rhs[1 + b], rr[r]);
+                    wc[b * Q + 1 + r] = dot(rhs[1 + b], rrw[r]) * sq;
 #pragma unroll
                 for (int r2 = 0; r2 <= r; ++r2) {
-                    const double v = dot(rr[r], rr[r2]);
+                    const double v = dot(rr[r], rrw[r2]) * rho_e;
                     cc[(1 + r) * Q + 1 + r2] = v;
                     cc[(1 + r2) * Q + 1 + r] = v;
                 }
             }
         }
-        const double logdet = log(pv_last);
+        const double logdet = log(d_e);
         const bool emit = active && failpiv == 0;
         // every lane evaluates every term (they are a handful of flops each) and keeps the ones it
         // owns (o mod G == lane); selects instead of L divergent branches
@@ -543,7 +565,7 @@ static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
 // Off-diagonal pair table of a tier, built once per (device, G, S) and kept for the process
 // lifetime: entry t = a << 24 | c << 16 | (a(a+1)/2 + c) for the t-th pair (a > c), pairs ordered
 // by descending c (so the pairs among the LAST k local points are the first k(k-1)/2 entries),
-// padded to a multiple of 2G with copies of the last pair.
+// padded to a multiple of NI*G (NI = 4 pairs in flight per lane) with copies of the last pair.
 static const unsigned int *tiled_pair_table(int G, int S)
 {
     static std::mutex mu;
@@ -556,7 +578,7 @@ static const unsigned int *tiled_pair_table(int G, int S)
     auto it = cache.find(key);
     if (it != cache.end())
         return it->second;
-    const int cap = G * S, toff = (cap - 1) * (cap - 2) / 2, tpad = (toff + 2 * G - 1) / (2 * G) * (2 * G);
+    const int cap = G * S, toff = (cap - 1) * (cap - 2) / 2, tpad = (toff + TILED_NI * G - 1) / (TILED_NI * G) * (TILED_NI * G);
     std::vector<unsigned int> host((size_t)tpad);
     int t = 0;
     for (int c = cap - 2; c >= 1; --c) // descending c: the pairs among the last k points come first
