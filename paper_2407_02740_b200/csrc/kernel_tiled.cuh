@@ -105,16 +105,19 @@ template <int G, int S, int D, int QD>
 struct TileSmem {
     using Geo = TileGeom<G, S>;
     static constexpr int DP = (D + 1) & ~1;                 // padded coordinate stride (16-byte rows)
-    static constexpr int PTS = Geo::CAP * DP;               // coordinates; reused for u after the build
-    static constexpr int DOFF = Geo::CAP * (Geo::CAP - 1) / 2; // packed strict lower triangle of one D_j
-    static constexpr int DSZ = (DOFF + 1 + 1) & ~1;         // + one zero slot (the diagonal of D_j)
+    static constexpr int PTS = Geo::CAP * DP;               // scaled coordinates of the local frame
+    // K staging, the column store of the factorization and every D_j share ONE packing: element
+    // (a, c), a >= c, at colbase(c) + a (columns back to back).  The pair table walks the columns
+    // from the last one down, rows ascending, so the staging stores of a lane group are contiguous;
+    // the row loads (static c, lane-varying a) are contiguous as well.
+    static constexpr int DSZ = (Geo::TRI + 1) & ~1;
     static constexpr int PER_OBS = PTS + Geo::KL + QD * DSZ;
     static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
     // Local row 0 is ALWAYS a padding row (tiers serve m+1 <= CAP-1), so nothing is computed for it.
     // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
-    // multiple of NI*G with copies of the last pair; entry = a << 24 | c << 16 | packed index tri(a)+c
+    // multiple of NI*G with copies of the last pair; entry = a << 24 | c << 16 | (colbase(c) + a)
     static constexpr int TOFF = (Geo::CAP - 1) * (Geo::CAP - 2) / 2; // pairs among local rows 1..CAP-1
-    static constexpr int NI = TILED_NI;                            // pairs in flight per lane in the pair loop
+    static constexpr int NI = TILED_NI;                     // pairs in flight per lane in the pair loop
     static constexpr int TPAD = (TOFF + NI * G - 1) / (NI * G) * (NI * G);
 };
 
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
     using FT = FamTraits<FAM, D>;
     constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
     using SM = TileSmem<G, S, D, QD>;
-    constexpr int DP = SM::DP, DSZ = SM::DSZ, DZERO = SM::DOFF;
+    constexpr int DP = SM::DP, DSZ = SM::DSZ;
     constexpr int L = (1 + Q) * (2 + P + P * P) + Q * Q;
     constexpr int NACC = (L + G - 1) / G;
     const AccLayout A(P, Q);
@@ -147,19 +150,17 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
 
     for (int t = lane; t < VB_EXPTAB; t += 32)
         etab[t] = exp2((double)t * (1.0 / VB_EXPTAB));
-    // zero slot (diagonal of D_j) and column 0 of D_j (padding row, never written by the pair loop)
+    // diagonal and column 0 of every D_j are zero and never written by the pair loop
 #pragma unroll
-    for (int j = 0; j < QD; ++j) {
-        if (lg == 0)
-            Dms[j * DSZ + DZERO] = 0.0;
-        for (int a = 1 + lg; a < CAP; a += G)
-            Dms[j * DSZ + a * (a - 1) / 2] = 0.0;
-    }
-    int rowi[S], tri_r[S], colb_r[S];
+    for (int j = 0; j < QD; ++j)
+        for (int a = lg; a < CAP; a += G) {
+            Dms[j * DSZ + a] = 0.0;
+            Dms[j * DSZ + Geo::colbase(a) + a] = 0.0;
+        }
+    int rowi[S], colb_r[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         rowi[s] = s * G + ((s & 1) ? (G - 1 - lg) : lg);
-        tri_r[s] = rowi[s] * (rowi[s] + 1) / 2;
         colb_r[s] = Geo::colbase(rowi[s]);
     }
     double acc[NACC];
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
 #pragma unroll
             for (int l = 0; l < DP; l += 2)
                 *reinterpret_cast<double2 *>(pts + a * DP + l) = make_double2(cx[l], cx[l + 1]);
-            KLs[tri_r[s] + a] = live ? E.diag : 1.0;
+            KLs[colb_r[s] + a] = live ? E.diag : 1.0;
             const unsigned bal = __ballot_sync(FULLMASK, live);
             nlive += __popc((G == 32) ? bal : ((bal >> (g * G)) & ((1u << (G & 31)) - 1u)));
         }
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                     KLs[kidx] = Kv[h];
 #pragma unroll
                     for (int j = 0; j < QD; ++j)
-                        Dms[j * DSZ + kidx - (int)(ent[h] >> 24)] = Dv[h][j];
+                        Dms[j * DSZ + kidx] = Dv[h][j];
                 }
             }
             __syncwarp();
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                 KLs[kidx] = 0.0;
 #pragma unroll
                 for (int j = 0; j < QD; ++j)
-                    Dms[j * DSZ + kidx - (int)(e0 >> 24)] = 0.0;
+                    Dms[j * DSZ + kidx] = 0.0;
             }
         }
         __syncwarp();
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int c = 0; c < (s + 1) * G; ++c)
-                Kr[s][c] = KLs[tri_r[s] + c];
+                Kr[s][c] = KLs[Geo::colbase(c) + rowi[s]];
         __syncwarp();
 
         // ---- square-root-free factorization K = Lt D Lt^T (Lt unit lower, D = diag(d)), right-looking,
@@ -371,8 +372,8 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
         //      sb_j = sum_{l>j} K(l,j) ut_l from the unscaled column store, ut_j = e_j - sb_j / d_j.  As
         //      soon as ut_l is known (and broadcast) it is also applied to the packed derivative
         //      matrices, tt_r += D_r[., l] ut_l, so D_r u needs no separate mat-vec pass.  Element
-        //      (a, l) of the symmetric D_r lives at a(a-1)/2 + l (a > l) or l(l-1)/2 + a (a < l); for
-        //      a == l the first form points at D[a+1][0], a column-0 entry, which is always zero. ----
+        //      (a, l) of the symmetric D_r lives at colbase(a) + l (a < l) or colbase(l) + a (a >= l;
+        //      the diagonal holds zeros). ----
         double sb[S], eb[S], rr[QD + 1][S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(con
                     const double Klj = above ? KLs[colb_r[s] + l] : 0.0;
                     sb[s] = fma(Klj, ul, sb[s]);
                 }
-                const int addr = above ? (l * (l - 1) / 2 + rowi[s]) : (tri_r[s] - rowi[s] + l);
+                const int addr = above ? (colb_r[s] + l) : (Geo::colbase(l) + rowi[s]);
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
                     rr[r][s] = fma(Dms[r * DSZ + addr], ul, rr[r][s]);
@@ -563,7 +564,7 @@ static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
 #include <vector>
 
 // Off-diagonal pair table of a tier, built once per (device, G, S) and kept for the process
-// lifetime: entry t = a << 24 | c << 16 | (a(a+1)/2 + c) for the t-th pair (a > c), pairs ordered
+// lifetime: entry t = a << 24 | c << 16 | (colbase(c) + a) for the t-th pair (a > c), pairs ordered
 // by descending c (so the pairs among the LAST k local points are the first k(k-1)/2 entries),
 // padded to a multiple of NI*G (NI = 4 pairs in flight per lane) with copies of the last pair.
 static const unsigned int *tiled_pair_table(int G, int S)
@@ -583,7 +584,7 @@ static const unsigned int *tiled_pair_table(int G, int S)
     int t = 0;
     for (int c = cap - 2; c >= 1; --c) // descending c: the pairs among the last k points come first
         for (int a = c + 1; a < cap; ++a)
-            host[t++] = ((unsigned)a << 24) | ((unsigned)c << 16) | (unsigned)(a * (a + 1) / 2 + c);
+            host[t++] = ((unsigned)a << 24) | ((unsigned)c << 16) | (unsigned)(c * (cap - 1) - c * (c - 1) / 2 + a);
     for (; t < tpad; ++t)
         host[t] = host[toff - 1];
     unsigned int *dptr = nullptr;
