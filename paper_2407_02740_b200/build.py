@@ -44,15 +44,35 @@ def _gxx() -> str:
     raise RuntimeError("g++ not found")
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> Path:
-    sources = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "vecchia_b200.h"]
-    if not force and _newer(CUDA_LIB, sources):
+def build_cuda(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+    """Compile csrc/vecchia_b200.cu and every csrc/gen/tiled_part_*.cu to objects (in parallel)
+    and link them into lib/libvecchia_b200.so.  sm_100a only, -lineinfo for ncu source pages."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    headers = sorted(CSRC.glob("*.cuh")) + sorted((CSRC / "gen").glob("*.inc")) + [ROOT / "include" / "vecchia_b200.h"]
+    units = [CSRC / "vecchia_b200.cu"] + sorted((CSRC / "gen").glob("tiled_part_*.cu"))
+    if not force and _newer(CUDA_LIB, headers + units):
         return CUDA_LIB
     LIBDIR.mkdir(exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(CUDA_LIB), str(CSRC / "vecchia_b200.cu")]
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-I", str(ROOT / "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+        flags.append("-Xptxas=-v")
+
+    def compile_one(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        if force or not _newer(obj, headers + [src]):
+            subprocess.run([nvcc, *flags, "-c", str(src), "-o", str(obj)], check=True)
+        return obj
+
+    jobs = jobs or min(len(units), os.cpu_count() or 1)
+    with ThreadPoolExecutor(max_workers=jobs) as pool:
+        objs = list(pool.map(compile_one, units))
+    subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(CUDA_LIB),
+                    *map(str, objs)], check=True)
     return CUDA_LIB
 
 

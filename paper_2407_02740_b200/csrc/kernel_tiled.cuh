@@ -121,13 +121,15 @@ struct TileSmem {
     static constexpr int TPAD = (TOFF + NI * G - 1) / (NI * G) * (NI * G);
 };
 
-// blocks per SM the register budget is tuned for (one warp per block): 3 warps per SM sub-partition
-#ifndef TILED_MIN_BLOCKS
-#define TILED_MIN_BLOCKS 12
-#endif
+// blocks per SM (one warp per block) the register budget of a tier is tuned for: the rows a lane
+// keeps in registers take G*S(S+1) 32-bit registers; 168 registers = 3 warps per SM sub-partition
+__host__ __device__ constexpr int tiled_min_blocks(int G, int S)
+{
+    return (G * S * (S + 1) <= 48) ? 16 : ((G * S * (S + 1) <= 96) ? 12 : 8);
+}
 
 template <int G, int S, int FAM, int D, int P>
-__global__ void __launch_bounds__(32, TILED_MIN_BLOCKS) vecchia_tiled_kernel(const EvalParams E)
+__global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kernel(const EvalParams E)
 {
     using Geo = TileGeom<G, S>;
     using FT = FamTraits<FAM, D>;
@@ -541,100 +543,3 @@ struct TiledInstance {
             TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
             "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                            \
     }
-
-#include "tiled_instances.inc"
-
-static inline const TiledInstance *tiled_find(int family, int mp1, int p, int d)
-{
-    const TiledInstance *best = nullptr;
-    for (const TiledInstance &t : kTiledInstances)
-        if (t.family == family && t.d == d && t.p == p && t.cap - 1 >= mp1 && (!best || t.cap < best->cap))
-            best = &t;
-    return best;
-}
-
-static inline bool tiled_supported(int family, int mp1, int p, int d, int /*q*/)
-{
-    return tiled_find(family, mp1, p, d) != nullptr;
-}
-
-#include <map>
-#include <mutex>
-#include <tuple>
-#include <vector>
-
-// Off-diagonal pair table of a tier, built once per (device, G, S) and kept for the process
-// lifetime: entry t = a << 24 | c << 16 | (colbase(c) + a) for the t-th pair (a > c), pairs ordered
-// by descending c (so the pairs among the LAST k local points are the first k(k-1)/2 entries),
-// padded to a multiple of NI*G (NI = 4 pairs in flight per lane) with copies of the last pair.
-static const unsigned int *tiled_pair_table(int G, int S)
-{
-    static std::mutex mu;
-    static std::map<std::tuple<int, int, int>, unsigned int *> cache;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess)
-        return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_tuple(dev, G, S);
-    auto it = cache.find(key);
-    if (it != cache.end())
-        return it->second;
-    const int cap = G * S, toff = (cap - 1) * (cap - 2) / 2, tpad = (toff + TILED_NI * G - 1) / (TILED_NI * G) * (TILED_NI * G);
-    std::vector<unsigned int> host((size_t)tpad);
-    int t = 0;
-    for (int c = cap - 2; c >= 1; --c) // descending c: the pairs among the last k points come first
-        for (int a = c + 1; a < cap; ++a)
-            host[t++] = ((unsigned)a << 24) | ((unsigned)c << 16) | (unsigned)(c * (cap - 1) - c * (c - 1) / 2 + a);
-    for (; t < tpad; ++t)
-        host[t] = host[toff - 1];
-    unsigned int *dptr = nullptr;
-    if (cudaMalloc(&dptr, sizeof(unsigned int) * tpad) != cudaSuccess)
-        return nullptr;
-    if (cudaMemcpy(dptr, host.data(), sizeof(unsigned int) * tpad, cudaMemcpyHostToDevice) != cudaSuccess) {
-        cudaFree(dptr);
-        return nullptr;
-    }
-    cache[key] = dptr;
-    return dptr;
-}
-
-// returns 0, -100 (CUDA error pending), or a VB200_E* code
-template <class PartialsFn>
-static int launch_tiled(cudaStream_t stream, int sm_count, size_t smem_optin, EvalParams &E, int *nblocks,
-                        const char **name, PartialsFn get_partials)
-{
-    const TiledInstance *t = tiled_find(E.family, E.mp1, E.p, E.d);
-    if (!t)
-        return -4;
-    const size_t smem = (size_t)t->smem_doubles * sizeof(double);
-    if (smem > smem_optin)
-        return -4;
-    if (cudaFuncSetAttribute(t->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return -100;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t->kernel, 32, smem) != cudaSuccess)
-        return -100;
-    if (per_sm < 1)
-        per_sm = 1;
-    const int opw = 32 / t->g;
-    const int64_t nbatch = (E.i1 - E.i0 + opw - 1) / opw;
-    int64_t blocks = (int64_t)sm_count * per_sm;
-    if (blocks > nbatch)
-        blocks = nbatch;
-    if (blocks < 1)
-        blocks = 1;
-    double *partials = get_partials((size_t)blocks * E.L);
-    if (!partials)
-        return -3;
-    E.partials = partials;
-    E.pair_tab = tiled_pair_table(t->g, t->s);
-    if (!E.pair_tab)
-        return -100;
-    cudaFuncSetAttribute(t->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    t->kernel<<<(unsigned)blocks, 32, smem, stream>>>(E);
-    if (cudaGetLastError() != cudaSuccess)
-        return -100;
-    *nblocks = (int)blocks;
-    *name = t->name;
-    return 0;
-}

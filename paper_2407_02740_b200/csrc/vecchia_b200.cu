@@ -11,7 +11,7 @@
 
 #include "common.cuh"
 #include "kernel_warp_smem.cuh"
-#include "kernel_tiled.cuh"
+#include "tiled_host.cuh"
 
 // ---------------------------------------------------------------------------
 // error plumbing
