@@ -145,6 +145,11 @@ int vb200_eval_rows(vb200_problem *prob, int family, const double *theta, int q,
 int vb200_last_launch_count(const vb200_problem *prob);
 const char *vb200_last_kernel_name(const vb200_problem *prob);
 
+/* Enumerate the compiled TILED_REG kernel instances (for tests and tooling): instance k serves
+ * `family` with exactly d coordinates and p design columns, for any m+1 <= cap-1. */
+int vb200_tiled_instance_count(void);
+int vb200_tiled_instance(int k, int *lanes_per_obs, int *rows_per_lane, int *cap, int *family, int *d, int *p);
+
 /* CUDA-event timing of the MAIN kernel only (not the reset / reduction launches): enable,
  * evaluate, then read the duration of the last main-kernel launch in milliseconds
  * (synchronises on the closing event).  Used by bench.py for roofline.achieved. */

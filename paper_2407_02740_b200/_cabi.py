@@ -39,6 +39,8 @@ _SIGNATURES = {
     "vb200_eval_rows": (c_int, [c_void_p, c_int, _dp, c_int, c_double, c_int64, c_int64, _dp, POINTER(c_int32)]),
     "vb200_last_launch_count": (c_int, [c_void_p]),
     "vb200_last_kernel_name": (c_char_p, [c_void_p]),
+    "vb200_tiled_instance_count": (c_int, []),
+    "vb200_tiled_instance": (c_int, [c_int] + [POINTER(c_int)] * 6),
     "vb200_enable_timing": (c_int, [c_void_p, c_int]),
     "vb200_last_kernel_ms": (c_int, [c_void_p, _dp]),
     "vb200_measure_fp64_peak": (c_int, [c_int, c_double, _dp, _dp]),
@@ -94,3 +96,14 @@ def check(rc: int, what: str = "") -> None:
 
 def device_count() -> int:
     return int(load().vb200_device_count())
+
+
+def tiled_instances():
+    """List of (lanes_per_obs, rows_per_lane, cap, family_code, d, p) of the compiled TILED_REG kernels."""
+    lib = load()
+    out = []
+    for k in range(lib.vb200_tiled_instance_count()):
+        vals = [c_int() for _ in range(6)]
+        check(lib.vb200_tiled_instance(k, *[ctypes.byref(v) for v in vals]), "vb200_tiled_instance")
+        out.append(tuple(v.value for v in vals))
+    return out

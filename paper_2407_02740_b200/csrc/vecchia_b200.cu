@@ -643,6 +643,32 @@ extern "C" int vb200_eval_rows(vb200_problem *P, int family, const double *theta
     return rc;
 }
 
+extern "C" int vb200_tiled_instance_count(void)
+{
+    int n = 0;
+    for (const TiledPart &part : kTiledParts)
+        n += *part.count;
+    return n;
+}
+
+extern "C" int vb200_tiled_instance(int k, int *g, int *s, int *cap, int *family, int *d, int *p)
+{
+    for (const TiledPart &part : kTiledParts) {
+        if (k < *part.count) {
+            const TiledInstance &t = part.items[k];
+            if (g) *g = t.g;
+            if (s) *s = t.s;
+            if (cap) *cap = t.cap;
+            if (family) *family = t.family;
+            if (d) *d = t.d;
+            if (p) *p = t.p;
+            return VB200_OK;
+        }
+        k -= *part.count;
+    }
+    return fail(VB200_EINVAL, "instance index out of range");
+}
+
 extern "C" int vb200_enable_timing(vb200_problem *P, int on)
 {
     if (!P)

@@ -178,6 +178,32 @@ def test_families_and_shapes_against_oracle(family, d, p, theta, m):
             assert np.array_equal(got, again), "device reduction must be run-to-run reproducible"
 
 
+def test_every_compiled_tiled_instance_against_oracle():
+    """Each TILED_REG kernel instance (tier x family x d x p), at the widest m it serves and at a
+    narrow one (heavy front padding), plus the ragged head rows, against the CPU oracle."""
+    from paper_2407_02740_b200 import _cabi
+    names = {0: "exponential_isotropic", 1: "exponential_anisotropic", 2: "exponential_spacetime",
+             3: "matern15_isotropic", 4: "matern25_isotropic"}
+    inst = _cabi.tiled_instances()
+    assert len(inst) >= 60
+    rng = np.random.default_rng(77)
+    for g, s_, cap, fam, d, p in inst:
+        family = names[fam]
+        q = _cabi.load().vb200_family_nparms(fam, d)
+        theta = np.concatenate([[1.3], rng.uniform(0.15, 0.4, q - 2), [0.08]])
+        for m in sorted({cap - 2, max(2, cap // 2 - 3)}):
+            n = 3 * cap + 40
+            y, X, locs, _ = make_instance(1000 + cap + d + p + m, n, d, p)
+            nn = vg.find_ordered_neighbors(locs, m)
+            want = vo.run(y, X, locs, nn.idx, family, theta)
+            with DeviceProblem(vg.Dataset(y, X, locs), nn, family) as prob:
+                prob.set_layout("tiled_reg")
+                got = prob.totals(theta)
+                if m == cap - 2:  # the widest m of the tier must be served by exactly this instance
+                    assert f"G={g},S={s_}," in prob.last_kernel_name, (prob.last_kernel_name, g, s_, m)
+                fields_close(got, want, p, q, 1e-9)
+
+
 def test_shard_sums_equal_whole_and_empty_range():
     y, X, locs, theta = make_instance(9, 5000, 2, 1)
     nn = vg.find_ordered_neighbors(locs, 30)
