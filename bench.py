@@ -299,7 +299,10 @@ def ours_arm(args):
     ee.record()
     torch.cuda.synchronize()
     barrier()
-    e2e_ms = max(es.elapsed_time(ee), 1000.0 * (time.perf_counter() - t0)) / e2e_steps
+    e2e_mean_ms = max(es.elapsed_time(ee), 1000.0 * (time.perf_counter() - t0)) / e2e_steps
+    # the per-step host wall times show occasional 2-4x outliers on these shared hosts (PCIe / host
+    # noise; the device work is constant): the headline uses the median step, the mean is reported too
+    e2e_ms = float(np.median(e2e_each))
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -338,7 +341,8 @@ def ours_arm(args):
         "data": "synthetic", "config": workload_config(args, n_total),
         "clocks": clocks.summary(),
         "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms, "steps": e2e_steps, "ms_each": [round(x, 2) for x in e2e_each],
+                "ms_per_step": e2e_ms, "ms_per_step_mean": e2e_mean_ms, "steps": e2e_steps,
+                "ms_each": [round(x, 2) for x in e2e_each], "statistic": "median of the per-step wall times",
                 "path": "engine.DeviceProblem(pinned host y/X/locs/nn) -> vb200_create -> vb200_eval_async -> host"},
         "gpu_launches": launches, "roofline": roofline,
         "loglik": ev.loglik, "neighbor_search_s": t_nn,
