@@ -343,7 +343,7 @@ def ours_arm(args):
         "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms, "ms_per_step_mean": e2e_mean_ms, "steps": e2e_steps,
                 "ms_each": [round(x, 2) for x in e2e_each], "statistic": "median of the per-step wall times",
-                "path": "engine.DeviceProblem(pinned host y/X/locs/nn) -> vb200_create -> vb200_eval_async -> host"},
+                "path": "engine.DeviceProblem(pinned host y/X/locs/nn): table uploaded in 8 chunks on a side stream, vb200_create + vb200_eval_async per chunk behind the copies -> totals on the host"},
         "gpu_launches": launches, "roofline": roofline,
         "loglik": ev.loglik, "neighbor_search_s": t_nn,
     }

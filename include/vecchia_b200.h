@@ -96,7 +96,8 @@ int vb200_device_count(void);                /* 0 when no usable CUDA device */
  * Each of y, X, locs, nn may be a HOST pointer (copied to the device here) or
  * a DEVICE pointer on `device` (adopted without a copy; the caller keeps it
  * alive until vb200_destroy -- this is how torch-allocated buffers are passed).
- * `stream` is a cudaStream_t (NULL = a private non-blocking stream).
+ * `stream` is a cudaStream_t; NULL is CUDA's default stream.  Device buffers passed in must be
+ * ready in stream order on `stream` (the library launches everything there).
  * Replaces the array arguments of the reference runners (_kernels.pyx:392-393).
  */
 int vb200_create(int device, int64_t n, int p, int d, int mp1,

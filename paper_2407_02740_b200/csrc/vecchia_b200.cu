@@ -213,10 +213,11 @@ extern "C" int vb200_create(int device, int64_t n, int p, int d, int mp1, const 
     P->nn_rows = nn_rows;
     int rc = VB200_OK;
     double *ty = nullptr, *tX = nullptr, *tl = nullptr;
-    auto cleanup_tmp = [&]() {
-        if (ty) cudaFree(ty);
-        if (tX) cudaFree(tX);
-        if (tl) cudaFree(tl);
+    auto cleanup_tmp = [&]() { // stream-ordered: freed after the pack kernel that reads them
+        if (ty) cudaFreeAsync(ty, P->stream);
+        if (tX) cudaFreeAsync(tX, P->stream);
+        if (tl) cudaFreeAsync(tl, P->stream);
+        ty = tX = tl = nullptr;
     };
 #define TRY_OR_FREE(expr)                                                                                \
     do {                                                                                                 \
@@ -230,34 +231,41 @@ extern "C" int vb200_create(int device, int64_t n, int p, int d, int mp1, const 
         }                                                                                                \
     } while (0)
 
-    if (stream) {
-        P->stream = (cudaStream_t)stream;
-    } else {
-        TRY_OR_FREE(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
-        P->own_stream = true;
+    // NULL is CUDA's (legacy) default stream, NOT a private one: work the caller queued on the
+    // default stream before this call (e.g. torch uploads of the input buffers) is ordered before
+    // everything the library launches.
+    P->stream = (cudaStream_t)stream;
+    {
+        int sms = 0, optin = 0; // cudaDeviceGetAttribute is cheap; cudaGetDeviceProperties takes milliseconds
+        TRY_OR_FREE(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        TRY_OR_FREE(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        P->sm_count = sms;
+        P->smem_optin = (size_t)optin;
     }
-    cudaDeviceProp prop;
-    TRY_OR_FREE(cudaGetDeviceProperties(&prop, device));
-    P->sm_count = prop.multiProcessorCount;
-    P->smem_optin = prop.sharedMemPerBlockOptin;
 
+    // Stream-ordered allocations (cudaMallocAsync / cudaFreeAsync): no device-wide synchronisation,
+    // so a caller that is still uploading the neighbor table on another stream keeps overlapping.
+    bool copied_from_host = false;
     const double *dy = y, *dX = X, *dl = locs;
     if (!is_device_ptr(y)) {
-        TRY_OR_FREE(cudaMalloc(&ty, sizeof(double) * n));
+        copied_from_host = true;
+        TRY_OR_FREE(cudaMallocAsync(&ty, sizeof(double) * n, P->stream));
         TRY_OR_FREE(cudaMemcpyAsync(ty, y, sizeof(double) * n, cudaMemcpyHostToDevice, P->stream));
         dy = ty;
     }
     if (!is_device_ptr(X)) {
-        TRY_OR_FREE(cudaMalloc(&tX, sizeof(double) * n * p));
+        copied_from_host = true;
+        TRY_OR_FREE(cudaMallocAsync(&tX, sizeof(double) * n * p, P->stream));
         TRY_OR_FREE(cudaMemcpyAsync(tX, X, sizeof(double) * n * p, cudaMemcpyHostToDevice, P->stream));
         dX = tX;
     }
     if (!is_device_ptr(locs)) {
-        TRY_OR_FREE(cudaMalloc(&tl, sizeof(double) * n * d));
+        copied_from_host = true;
+        TRY_OR_FREE(cudaMallocAsync(&tl, sizeof(double) * n * d, P->stream));
         TRY_OR_FREE(cudaMemcpyAsync(tl, locs, sizeof(double) * n * d, cudaMemcpyHostToDevice, P->stream));
         dl = tl;
     }
-    TRY_OR_FREE(cudaMalloc(&P->rec, sizeof(double) * n * P->rs));
+    TRY_OR_FREE(cudaMallocAsync(&P->rec, sizeof(double) * n * P->rs, P->stream));
     {
         const int bs = 256;
         const unsigned grid = (unsigned)((n + bs - 1) / bs);
@@ -269,18 +277,20 @@ extern "C" int vb200_create(int device, int64_t n, int p, int d, int mp1, const 
     } else {
         int64_t *tn = nullptr;
         const size_t bytes = sizeof(int64_t) * (size_t)(nn_rows > 0 ? nn_rows : 1) * mp1;
-        TRY_OR_FREE(cudaMalloc(&tn, bytes));
+        copied_from_host = true;
+        TRY_OR_FREE(cudaMallocAsync(&tn, bytes, P->stream));
         P->nn = tn;
         P->own_nn = true;
         if (nn_rows > 0)
             TRY_OR_FREE(cudaMemcpyAsync(tn, nn, sizeof(int64_t) * (size_t)nn_rows * mp1, cudaMemcpyHostToDevice,
                                         P->stream));
     }
-    TRY_OR_FREE(cudaMalloc(&P->fail_word, sizeof(unsigned long long)));
-    TRY_OR_FREE(cudaMalloc(&P->fail_count, sizeof(unsigned int)));
-    TRY_OR_FREE(cudaMallocHost(&P->h_fail, sizeof(unsigned long long)));
-    TRY_OR_FREE(cudaStreamSynchronize(P->stream));
+    TRY_OR_FREE(cudaMallocAsync(&P->fail_word, 2 * sizeof(unsigned long long), P->stream));
+    P->fail_count = reinterpret_cast<unsigned int *>(P->fail_word + 1);
     cleanup_tmp();
+    // host inputs may be released by the caller on return; adopted device inputs need no wait
+    if (copied_from_host)
+        TRY_OR_FREE(cudaStreamSynchronize(P->stream));
 #undef TRY_OR_FREE
     *out = P;
     return VB200_OK;
@@ -291,19 +301,16 @@ extern "C" int vb200_destroy(vb200_problem *P)
     if (!P)
         return VB200_OK;
     cudaSetDevice(P->device);
-    if (P->stream)
-        cudaStreamSynchronize(P->stream);
-    if (P->rec) cudaFree(P->rec);
-    if (P->own_nn && P->nn) cudaFree((void *)P->nn);
-    if (P->partials) cudaFree(P->partials);
-    if (P->d_out) cudaFree(P->d_out);
-    if (P->fail_word) cudaFree(P->fail_word);
-    if (P->fail_count) cudaFree(P->fail_count);
+    cudaStreamSynchronize(P->stream);
+    if (P->rec) cudaFreeAsync(P->rec, P->stream);
+    if (P->own_nn && P->nn) cudaFreeAsync((void *)P->nn, P->stream);
+    if (P->partials) cudaFreeAsync(P->partials, P->stream);
+    if (P->d_out) cudaFreeAsync(P->d_out, P->stream);
+    if (P->fail_word) cudaFreeAsync(P->fail_word, P->stream);
     if (P->h_out) cudaFreeHost(P->h_out);
     if (P->h_fail) cudaFreeHost(P->h_fail);
     if (P->ev0) cudaEventDestroy(P->ev0);
     if (P->ev1) cudaEventDestroy(P->ev1);
-    if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
     cudaGetLastError();
     delete P;
     return VB200_OK;
@@ -314,11 +321,7 @@ extern "C" int vb200_set_stream(vb200_problem *P, void *stream)
     if (!P)
         return fail(VB200_EINVAL, "NULL problem");
     cudaSetDevice(P->device);
-    if (P->stream)
-        cudaStreamSynchronize(P->stream);
-    if (P->own_stream && P->stream)
-        cudaStreamDestroy(P->stream);
-    P->own_stream = false;
+    cudaStreamSynchronize(P->stream); // buffers were allocated in the old stream's order
     P->stream = (cudaStream_t)stream;
     return VB200_OK;
 }
@@ -401,10 +404,10 @@ static int ensure_partials(vb200_problem *P, size_t doubles)
     if (doubles <= P->partials_cap)
         return VB200_OK;
     if (P->partials)
-        cudaFree(P->partials);
+        cudaFreeAsync(P->partials, P->stream);
     P->partials = nullptr;
     P->partials_cap = 0;
-    CUDA_TRY(cudaMalloc(&P->partials, sizeof(double) * doubles));
+    CUDA_TRY(cudaMallocAsync(&P->partials, sizeof(double) * doubles, P->stream));
     P->partials_cap = doubles;
     return VB200_OK;
 }
@@ -542,11 +545,20 @@ extern "C" int vb200_sync(vb200_problem *P)
     return VB200_OK;
 }
 
+static int ensure_host_fail(vb200_problem *P)
+{
+    if (!P->h_fail)
+        CUDA_TRY(cudaMallocHost(&P->h_fail, sizeof(unsigned long long)));
+    return VB200_OK;
+}
+
 extern "C" int vb200_fail_info(vb200_problem *P, int64_t *first_fail, int32_t *pivot)
 {
     if (!P)
         return fail(VB200_EINVAL, "NULL problem");
     CUDA_TRY(cudaSetDevice(P->device));
+    if (int rc0 = ensure_host_fail(P))
+        return rc0;
     CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
@@ -587,6 +599,8 @@ extern "C" int vb200_eval(vb200_problem *P, int family, const double *theta, int
         CUDA_TRY(cudaMallocHost(&P->h_out, sizeof(double) * (L + 2)));
         P->h_out_cap = L + 2;
     }
+    if (int rc0 = ensure_host_fail(P))
+        return rc0;
     int rc = enqueue_eval(P, family, theta, q, jitter, i0, i1, P->d_out, nullptr, nullptr);
     if (rc)
         return rc;

@@ -112,9 +112,15 @@ class DeviceProblem:
     """
 
     def __init__(self, ds: Dataset, nn: NeighborArray, family: str, device=None, row0: int = 0,
-                 rows: int | None = None, layout: str = "auto", nn_is_shard: bool = False):
+                 rows: int | None = None, layout: str = "auto", nn_is_shard: bool = False,
+                 upload_chunks: int | None = None):
         """``nn`` is the full (n, m+1) table, or -- with ``nn_is_shard`` -- only its rows
-        [row0, row0+rows) (what each rank of a sharded run builds for itself)."""
+        [row0, row0+rows) (what each rank of a sharded run builds for itself).
+
+        The neighbor table is by far the largest input (8(m+1) bytes per observation).  It is
+        uploaded in ``upload_chunks`` pieces on a side stream, and the FIRST evaluation is issued
+        chunk by chunk behind the copies (the C ABI evaluates any row range), so host-to-device
+        transfer and compute overlap; later evaluations see a fully resident table."""
         torch = _torch()
         lib = _cabi.load()
         fam = covariance_registry(family)
@@ -131,12 +137,36 @@ class DeviceProblem:
         self.row0, self.rows = row0, rows
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         with torch.cuda.device(self.device):
-            stream = torch.cuda.current_stream()
+            # A private (non-blocking) stream: the legacy default stream would serialise the library's
+            # work against the side-stream upload of the neighbor table.  Consumers on other streams are
+            # ordered behind it with an event (see _publish).
+            self._stream = torch.cuda.Stream(device=self.device)
+        with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+            stream = self._stream
             put = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=True)
             self._y, self._X, self._locs = put(ds.y), put(ds.X), put(work)
-            self._nn = put(shard_rows) if rows > 0 else torch.zeros((1, self.mp1), dtype=torch.int64,
-                                                                                  device=self.device)
+            self._pending = []  # (first_row, end_row, event) of table chunks whose upload may be in flight
+            if upload_chunks is None:
+                upload_chunks = 8 if rows * self.mp1 * 8 >= (32 << 20) else 1
+            if rows > 0 and upload_chunks > 1:
+                host_nn = torch.from_numpy(np.ascontiguousarray(shard_rows))
+                self._nn = torch.empty((rows, self.mp1), dtype=torch.int64, device=self.device)
+                side = torch.cuda.Stream(device=self.device)
+                self._nn.record_stream(side)
+                cuts = np.linspace(0, rows, upload_chunks + 1).astype(np.int64)
+                with torch.cuda.stream(side):
+                    for a, b in zip(cuts[:-1], cuts[1:]):
+                        if b > a:
+                            self._nn[a:b].copy_(host_nn[a:b], non_blocking=True)
+                            ev = torch.cuda.Event()
+                            ev.record(side)
+                            self._pending.append((row0 + int(a), row0 + int(b), ev))
+                self._host_nn = host_nn  # keep the source alive while the copies run
+            else:
+                self._nn = put(shard_rows) if rows > 0 else torch.zeros((1, self.mp1), dtype=torch.int64,
+                                                                        device=self.device)
             self._out = torch.zeros(acc_len(p, VB_MAX_Q) + 2, dtype=torch.float64, device=self.device)
+            self._out_chunks = None
             handle = ctypes.c_void_p()
             rc = lib.vb200_create(self.device.index or 0, n, p, self.d, self.mp1, self._y.data_ptr(),
                                   self._X.data_ptr(), self._locs.data_ptr(), self._nn.data_ptr(), row0, rows,
@@ -150,6 +180,8 @@ class DeviceProblem:
     # -- lifetime ---------------------------------------------------------------
     def close(self):
         if getattr(self, "_h", None) is not None and self._h:
+            if getattr(self, "_pending", None):
+                self._settle_uploads()  # never free buffers under a copy that is still in flight
             self._lib.vb200_destroy(self._h)
             self._h = None
 
@@ -173,10 +205,23 @@ class DeviceProblem:
         return _cabi.LAYOUT_NAMES[self._lib.vb200_get_layout(self._h, self.kernel_code, q)]
 
     def use_current_stream(self):
+        """Launch on torch's current stream from now on (so that torch CUDA events bracket the kernels)."""
         torch = _torch()
+        if self._pending:
+            self._settle_uploads()
         with torch.cuda.device(self.device):
-            s = torch.cuda.current_stream().cuda_stream
-        _cabi.check(self._lib.vb200_set_stream(self._h, ctypes.c_void_p(s)), "vb200_set_stream")
+            self._stream = torch.cuda.current_stream()
+        _cabi.check(self._lib.vb200_set_stream(self._h, ctypes.c_void_p(self._stream.cuda_stream)),
+                    "vb200_set_stream")
+
+    def _publish(self):
+        """Order torch's current stream behind everything enqueued on the problem's stream."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self._stream:
+            ev = torch.cuda.Event()
+            ev.record(self._stream)
+            cur.wait_event(ev)
 
     def enable_timing(self, on: bool = True):
         _cabi.check(self._lib.vb200_enable_timing(self._h, int(on)), "vb200_enable_timing")
@@ -205,6 +250,12 @@ class DeviceProblem:
         q = th.shape[0]
         i0 = self.row0 if i0 is None else i0
         i1 = self.row0 + self.rows if i1 is None else i1
+        if self._pending:  # first evaluation: run it behind the chunked upload
+            L = acc_len(self.p, q)
+            host = self.totals_async(th, jitter, i0, i1).cpu().numpy()
+            if host[L] == 0.0:
+                return host[:L].copy()
+            self._settle_uploads()  # a failure: fall through to the plain path for (observation, pivot)
         out = np.empty(acc_len(self.p, q))
         first, piv = ctypes.c_int64(-1), ctypes.c_int32(-1)
         rc = self._lib.vb200_eval(self._h, self.kernel_code, thp, q, float(jitter), int(i0), int(i1),
@@ -223,18 +274,65 @@ class DeviceProblem:
         i0 = self.row0 if i0 is None else i0
         i1 = self.row0 + self.rows if i1 is None else i1
         L = acc_len(self.p, q)
+        if self._pending:
+            return self._totals_behind_upload(thp, q, float(jitter), int(i0), int(i1), L)
         rc = self._lib.vb200_eval_async(self._h, self.kernel_code, thp, q, float(jitter), int(i0), int(i1),
                                         ctypes.c_void_p(self._out.data_ptr()))
         _cabi.check(rc, "vb200_eval_async")
+        self._publish()
+        return self._out[:L + 2]
+
+    def _settle_uploads(self):
+        torch = _torch()
+        with torch.cuda.device(self.device):
+            for _, _, ev in self._pending:
+                ev.synchronize()
+        self._pending = []
+        self._host_nn = None
+
+    def _totals_behind_upload(self, thp, q, jitter, i0, i1, L):
+        """Evaluate [i0, i1) one upload chunk at a time, each piece waiting (on the device) for its
+        chunk's copy event; the pieces' (L+2) vectors are combined on the device."""
+        torch = _torch()
+        with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+            compute = self._stream
+            if self._out_chunks is None or self._out_chunks.shape[0] < len(self._pending):
+                self._out_chunks = torch.zeros((len(self._pending), self._out.shape[0]), dtype=torch.float64,
+                                               device=self.device)
+            k = 0
+            for a, b, ev in self._pending:
+                lo, hi = max(a, i0), min(b, i1)
+                if lo >= hi:
+                    continue
+                compute.wait_event(ev)
+                rc = self._lib.vb200_eval_async(self._h, self.kernel_code, thp, q, jitter, lo, hi,
+                                                ctypes.c_void_p(self._out_chunks[k].data_ptr()))
+                _cabi.check(rc, "vb200_eval_async")
+                k += 1
+            if k == 0:
+                self._out[:L + 2] = torch.tensor([0.0] * (L + 1) + [float("-inf")], dtype=torch.float64,
+                                                 device=self.device)
+            else:
+                pieces = self._out_chunks[:k]
+                self._out[:L + 1] = pieces[:, :L + 1].sum(dim=0)
+                self._out[L + 1] = pieces[:, L + 1].max()
+            if i0 <= self.row0 and i1 >= self.row0 + self.rows:
+                # the compute stream now sits behind every copy: later work needs no more waits
+                self._pending = []
+        self._publish()
         return self._out[:L + 2]
 
     def fail_info(self):
+        if self._pending:
+            self._settle_uploads()
         first, piv = ctypes.c_int64(-1), ctypes.c_int32(-1)
         _cabi.check(self._lib.vb200_fail_info(self._h, ctypes.byref(first), ctypes.byref(piv)), "vb200_fail_info")
         return first.value, piv.value
 
     def rows_host(self, theta, jitter: float = 0.0, i0: int | None = None, i1: int | None = None):
         """Per-observation accumulator rows (i1-i0, L) and pivot+1 failure flags (diagnostics)."""
+        if self._pending:
+            self._settle_uploads()
         th, thp = self._theta(theta)
         q = th.shape[0]
         i0 = self.row0 if i0 is None else i0

@@ -292,8 +292,10 @@ def test_full_size_properties_n2_20():
     theta = np.array([1.0, 0.002, 0.1])
     nn = vg.find_ordered_neighbors(locs, m)
     with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern15_isotropic") as prob:
-        whole = prob.totals(theta)
-        assert np.array_equal(whole, prob.totals(theta))
+        first = prob.totals(theta)   # issued chunk by chunk behind the table upload
+        whole = prob.totals(theta)   # table resident: one launch
+        assert np.array_equal(whole, prob.totals(theta)), "resident evaluations must be bit-reproducible"
+        fields_close(first, whole, 1, 3, 1e-13)
         halves = prob.totals(theta, i1=n // 3) + prob.totals(theta, i0=n // 3)
         fields_close(halves, whole, 1, 3, 1e-11)
         P = vo.split_acc(whole, 1, 3)

@@ -14,14 +14,12 @@ nn = find_ordered_neighbor_rows(locs, m, 0, n)
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 hy, hX, hl, hn = pin(y), pin(X), pin(locs), pin(nn)
 ds = vg.Dataset(hy.numpy(), hX.numpy(), hl.numpy()); table = vg.NeighborArray(hn.numpy())
+print("views pinned?", torch.from_numpy(table.idx).is_pinned(), torch.from_numpy(ds.y).is_pinned())
 theta = np.array([1.0, 0.05, 0.1])
 def sync(): torch.cuda.synchronize()
-for rep in range(4):
-    t0 = time.perf_counter(); prob = engine.DeviceProblem(ds, table, "matern15_isotropic"); sync(); t1 = time.perf_counter()
+for chunks in (1, 8, 8, 1, 16, 4):
+    sync(); t0 = time.perf_counter()
+    prob = engine.DeviceProblem(ds, table, "matern15_isotropic", upload_chunks=chunks); t1 = time.perf_counter()
     tot = prob.totals(theta); t2 = time.perf_counter()
     prob.close(); sync(); t3 = time.perf_counter()
-    print(f"rep {rep}: create {1e3*(t1-t0):.2f} ms  eval {1e3*(t2-t1):.2f} ms  close {1e3*(t3-t2):.2f} ms")
-# raw copies
-for rep in range(3):
-    sync(); t0 = time.perf_counter(); d = hn.to("cuda", non_blocking=True); sync(); t1 = time.perf_counter()
-    print(f"nn H2D {hn.numel()*8/1e6:.0f} MB: {1e3*(t1-t0):.2f} ms = {hn.numel()*8/1e9/(t1-t0):.1f} GB/s"); del d
+    print(f"chunks {chunks}: create {1e3*(t1-t0):.2f} ms  eval {1e3*(t2-t1):.2f} ms  close {1e3*(t3-t2):.2f} ms  total {1e3*(t3-t0):.2f}")
