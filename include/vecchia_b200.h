@@ -62,13 +62,17 @@ extern "C" {
  *   EXP_ANISO                     : [variance, range_1..range_d, nugget]   (q = d+2)
  *   EXP_SPACETIME                 : [variance, range_space, range_time, nugget] (q = 4),
  *                                   time is the LAST coordinate
+ *   MATERN                        : [variance, range, smoothness, nugget]  (q = 4): general-order Matern
+ *                                   variance 2^(1-nu)/Gamma(nu) x^nu K_nu(x), x = r/range; the smoothness
+ *                                   derivative is a central difference of step 1e-5
  * The nugget is relative: diag = variance*(1+nugget) + jitter (_kernels.pyx:34-50). */
 enum vb200_family {
     VB200_EXP_ISO = 0,
     VB200_EXP_ANISO = 1,
     VB200_EXP_SPACETIME = 2,
     VB200_MATERN15 = 3,
-    VB200_MATERN25 = 4
+    VB200_MATERN25 = 4,
+    VB200_MATERN = 5
 };
 
 /* kernel layouts (the north-star layout study); AUTO picks the fastest that supports the shape */

@@ -15,6 +15,10 @@ Covariance definitions (relative nugget: diag = variance*(1+nugget) + jitter):
                           time is the last coordinate)
   matern15_isotropic      UNPINNED: variance*(1+x)exp(-x), x = r/range
   matern25_isotropic      UNPINNED: variance*(1+x+x^2/3)exp(-x)
+  matern_isotropic        UNPINNED: theta = variance, range, smoothness, nugget;
+                          variance * 2^(1-nu)/Gamma(nu) x^nu K_nu(x) with scipy.special.kv;
+                          range derivative analytic (variance*nc*x^(nu+1) K_{nu-1}(x)/range),
+                          smoothness derivative = central difference of step 1e-5
 """
 from __future__ import annotations
 
@@ -29,6 +33,16 @@ def _dist(pts):
     return np.sqrt((diff * diff).sum(axis=2))
 
 
+MATERN_H = 1e-5
+
+
+def _matern_corr(nu, x):
+    from scipy.special import gammaln, kv
+    with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+        out = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + nu * np.log(x)) * kv(nu, x)
+    return np.where(x < 1e-60, 1.0, out)
+
+
 def cov_and_derivs(family, theta, pts, jitter=0.0):
     """K (k,k) and the derivative stack D (q,k,k) at local points pts (k,d)."""
     theta = np.asarray(theta, dtype=np.float64)
@@ -37,7 +51,16 @@ def cov_and_derivs(family, theta, pts, jitter=0.0):
     sig2, tau2 = theta[0], theta[-1]
     eye = np.eye(k)
     D = np.zeros((q, k, k))
-    if family in ("exponential_isotropic", "exponential_sphere", "matern15_isotropic", "matern25_isotropic"):
+    if family == "matern_isotropic":
+        from scipy.special import gammaln, kv
+        rho, nu = theta[1], theta[2]
+        x = _dist(pts) / rho
+        corr = _matern_corr(nu, x)
+        with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+            drho = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + (nu + 1.0) * np.log(x)) * kv(nu - 1.0, x) / rho
+        D[1] = sig2 * np.where(x < 1e-60, 0.0, drho)
+        D[2] = sig2 * (_matern_corr(nu + MATERN_H, x) - _matern_corr(nu - MATERN_H, x)) / (2.0 * MATERN_H)
+    elif family in ("exponential_isotropic", "exponential_sphere", "matern15_isotropic", "matern25_isotropic"):
         rho = theta[1]
         x = _dist(pts) / rho
         e = np.exp(-x)

@@ -51,8 +51,11 @@ enum {
     FAM_EXP_ANISO = 1,
     FAM_EXP_SPACETIME = 2,
     FAM_MATERN15 = 3,
-    FAM_MATERN25 = 4
+    FAM_MATERN25 = 4,
+    FAM_MATERN = 5 /* general order: theta = variance, range, smoothness, nugget */
 };
+
+#define MATERN_H 1e-5 /* central-difference step of the smoothness derivative */
 
 typedef struct {
     const double *y, *X, *locs;
@@ -102,6 +105,105 @@ static double sq_dist_spacetime(const double *a, const double *b, int d, const d
     return s;
 }
 
+/* ---- general-order Matern (PARITY UNPINNED: not in the reference) ------------
+ * Modified Bessel function K_nu(x), real nu >= 0, x > 0, by Temme's method
+ * (J. Comput. Phys. 19, 1975): power series for x <= 2, Steed's continued
+ * fraction for x > 2, then upward recurrence in the order.  Written for the
+ * oracle independently of the device code; tests/test_oracle_golden.py checks
+ * it against scipy.special.kv. */
+static void temme_gammas(double mu, double *g1, double *g2, double *gpl, double *gmi)
+{
+    long double m = (long double)mu;
+    long double gp = 1.0L / tgammal(1.0L + m), gm = 1.0L / tgammal(1.0L - m);
+    *gpl = (double)gp;
+    *gmi = (double)gm;
+    *g2 = (double)((gm + gp) / 2.0L);
+    if (fabsl(m) < 1e-4L)
+        *g1 = (double)(-(0.5772156649015328606L - 0.0420026350340952L * m * m));
+    else
+        *g1 = (double)((gm - gp) / (2.0L * m));
+}
+
+static double bessel_k(double nu, double x, double *k_lower /* K_{nu-1} */)
+{
+    const int n = (int)floor(nu + 0.5);
+    const double mu = nu - n;
+    double kmu, kmu1;
+    if (x <= 2.0) {
+        double g1, g2, gpl, gmi;
+        temme_gammas(mu, &g1, &g2, &gpl, &gmi);
+        const double pimu = 3.14159265358979323846 * mu;
+        const double fact = fabs(pimu) < 1e-9 ? 1.0 : pimu / sin(pimu);
+        const double half = x / 2.0;
+        const double dl = -log(half);
+        double e = mu * dl;
+        const double sh = fabs(e) < 1e-10 ? 1.0 : sinh(e) / e;
+        double f = fact * (g1 * cosh(e) + g2 * sh * dl);
+        double s0 = f;
+        e = exp(e);
+        double pp = e / (2.0 * gpl), qq = 1.0 / (2.0 * e * gmi), cc = 1.0, s1 = pp;
+        for (int i = 1; i < 400; ++i) {
+            f = (i * f + pp + qq) / (i * i - mu * mu);
+            cc *= half * half / i;
+            pp /= (i - mu);
+            qq /= (i + mu);
+            double term = cc * f;
+            s0 += term;
+            s1 += cc * (pp - i * f);
+            if (fabs(term) < fabs(s0) * 1e-17)
+                break;
+        }
+        kmu = s0;
+        kmu1 = s1 * 2.0 / x;
+    } else {
+        double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, dh = d, q1 = 0.0, q2 = 1.0;
+        const double a1 = 0.25 - mu * mu;
+        double q = a1, c = a1, a = -a1, s = 1.0 + q * dh;
+        for (int i = 2; i < 400; ++i) {
+            a -= 2.0 * (i - 1);
+            c = -a * c / i;
+            double qn = (q1 - b * q2) / a;
+            q1 = q2;
+            q2 = qn;
+            q += c * qn;
+            b += 2.0;
+            d = 1.0 / (b + a * d);
+            dh = (b * d - 1.0) * dh;
+            h += dh;
+            double ds = q * dh;
+            s += ds;
+            if (fabs(ds) < fabs(s) * 1e-17)
+                break;
+        }
+        kmu = sqrt(3.14159265358979323846 / (2.0 * x)) * exp(-x) / s;
+        kmu1 = kmu * (mu + x + 0.5 - a1 * h) / x;
+    }
+    if (n == 0) {
+        if (k_lower)
+            *k_lower = kmu1 - (2.0 * mu / x) * kmu;
+        return kmu;
+    }
+    double lo = kmu, hi = kmu1;
+    for (int i = 1; i < n; ++i) {
+        double up = lo + (2.0 * (mu + i) / x) * hi;
+        lo = hi;
+        hi = up;
+    }
+    if (k_lower)
+        *k_lower = lo;
+    return hi;
+}
+
+static double matern_corr(double nu, double x)
+{
+    if (x < 1e-60)
+        return 1.0;
+    return exp((1.0 - nu) * 0.69314718055994530942 - lgamma(nu) + nu * log(x)) * bessel_k(nu, x, NULL);
+}
+
+/* exported for the tests */
+double vo_bessel_k(double nu, double x) { return bessel_k(nu, x, NULL); }
+
 static double pair_cov(const problem_t *P, const double *a, const double *b, int same)
 {
     const double *th = P->theta;
@@ -118,6 +220,8 @@ static double pair_cov(const problem_t *P, const double *a, const double *b, int
         double x = sqrt(sq_dist(a, b, P->d)) / th[1];
         return th[0] * (1.0 + x) * exp(-x);
     }
+    case FAM_MATERN:
+        return th[0] * matern_corr(th[2], sqrt(sq_dist(a, b, P->d)) / th[1]);
     default: { /* FAM_MATERN25 */
         double x = sqrt(sq_dist(a, b, P->d)) / th[1];
         return th[0] * (1.0 + x + x * x / 3.0) * exp(-x);
@@ -146,6 +250,8 @@ static double pair_dcov(const problem_t *P, int j, const double *a, const double
             double x = sqrt(sq_dist(a, b, d)) / th[1];
             return (1.0 + x) * exp(-x);
         }
+        case FAM_MATERN:
+            return matern_corr(th[2], sqrt(sq_dist(a, b, d)) / th[1]);
         default: {
             double x = sqrt(sq_dist(a, b, d)) / th[1];
             return (1.0 + x + x * x / 3.0) * exp(-x);
@@ -188,6 +294,18 @@ static double pair_dcov(const problem_t *P, int j, const double *a, const double
     case FAM_MATERN15: {
         double x = sqrt(sq_dist(a, b, d)) / th[1];
         return th[0] * x * x * exp(-x) / th[1];
+    }
+    case FAM_MATERN: {
+        double x = sqrt(sq_dist(a, b, d)) / th[1], nu = th[2];
+        if (x < 1e-60)
+            return 0.0;
+        if (j == 1) { /* d/d range = variance * nc * x^(nu+1) K_{nu-1}(x) / range */
+            double klow;
+            bessel_k(nu, x, &klow);
+            return th[0] * exp((1.0 - nu) * 0.69314718055994530942 - lgamma(nu) + (nu + 1.0) * log(x)) * klow / th[1];
+        }
+        /* j == 2: smoothness, central difference */
+        return th[0] * (matern_corr(nu + MATERN_H, x) - matern_corr(nu - MATERN_H, x)) / (2.0 * MATERN_H);
     }
     default: {
         double x = sqrt(sq_dist(a, b, d)) / th[1];

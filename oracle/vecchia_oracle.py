@@ -25,6 +25,7 @@ FAMILY_CODES = {
     "exponential_spacetime": 2,
     "matern15_isotropic": 3,
     "matern25_isotropic": 4,
+    "matern_isotropic": 5,  # general order: variance, range, smoothness, nugget
 }
 
 _c_dp = ctypes.POINTER(ctypes.c_double)
@@ -60,6 +61,8 @@ def lib():
             _c_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_int64,
             ctypes.c_int, _c_dp, _c_i32p,
         ]
+        L.vo_bessel_k.restype = ctypes.c_double
+        L.vo_bessel_k.argtypes = [ctypes.c_double, ctypes.c_double]
         L.vo_neighbor_scan.restype = None
         L.vo_neighbor_scan.argtypes = [_c_dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_i64p]
         _lib = L

@@ -12,6 +12,9 @@ adds the families BASELINE.json names that the reference lacks (SURVEY.md sectio
                              coordinate                                 code 2
     matern15_isotropic       [variance, range, nugget], nu = 3/2        code 3
     matern25_isotropic       [variance, range, nugget], nu = 5/2        code 4
+    matern_isotropic         [variance, range, smoothness, nugget], general order (Bessel K on the
+                             device by Temme's method; smoothness derivative by central difference)
+                                                                        code 5
 
 The nugget is relative: every diagonal entry is variance * (1 + nugget).
 The dense ``matrix`` / ``derivatives`` / ``cross`` helpers below are small-n host
@@ -32,6 +35,8 @@ KERNEL_ANISOTROPIC = 1
 KERNEL_SPACETIME = 2
 KERNEL_MATERN15 = 3
 KERNEL_MATERN25 = 4
+KERNEL_MATERN = 5
+MATERN_H = 1e-5  # smoothness central-difference step (csrc/common.cuh VB_MATERN_H)
 
 FAMILY_NAMES = (
     "exponential_isotropic",
@@ -40,6 +45,7 @@ FAMILY_NAMES = (
     "exponential_spacetime",
     "matern15_isotropic",
     "matern25_isotropic",
+    "matern_isotropic",
 )
 
 _CODES = {
@@ -49,6 +55,7 @@ _CODES = {
     "exponential_spacetime": KERNEL_SPACETIME,
     "matern15_isotropic": KERNEL_MATERN15,
     "matern25_isotropic": KERNEL_MATERN25,
+    "matern_isotropic": KERNEL_MATERN,
 }
 
 
@@ -65,7 +72,16 @@ def _scaled_distance(a, b, rho):
     return np.sqrt(np.einsum("ijk,ijk->ij", diff, diff)), diff
 
 
-def _correlation(code, x):
+def _matern_corr(nu, x):
+    from scipy.special import gammaln, kv
+    with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+        out = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + nu * np.log(x)) * kv(nu, x)
+    return np.where(x < 1e-60, 1.0, out)
+
+
+def _correlation(code, x, nu=None):
+    if code == KERNEL_MATERN:
+        return _matern_corr(nu, x)
     e = np.exp(-x)
     if code == KERNEL_MATERN15:
         return (1.0 + x) * e
@@ -84,7 +100,7 @@ class CovarianceFamily:
     def nparms(self, d: int) -> int:
         if self.name == "exponential_anisotropic":
             return d + 2
-        if self.name == "exponential_spacetime":
+        if self.name in ("exponential_spacetime", "matern_isotropic"):
             return 4
         return 3
 
@@ -103,7 +119,7 @@ class CovarianceFamily:
         theta = np.asarray(theta, dtype=np.float64)
         w = self.prepare_locs(np.atleast_2d(locs))
         s, _ = _scaled_distance(w, w, _axis_ranges(self.name, theta, w.shape[1]))
-        K = theta[0] * _correlation(self.kernel_code, s)
+        K = theta[0] * _correlation(self.kernel_code, s, theta[2] if self.kernel_code == KERNEL_MATERN else None)
         np.fill_diagonal(K, theta[0] * (1.0 + theta[-1]))
         return K
 
@@ -117,7 +133,8 @@ class CovarianceFamily:
         sig2, tau2 = theta[0], theta[-1]
         q = self.nparms(d)
         D = np.zeros((q, k, k))
-        D[0] = _correlation(self.kernel_code, s)
+        nu = theta[2] if self.kernel_code == KERNEL_MATERN else None
+        D[0] = _correlation(self.kernel_code, s, nu)
         np.fill_diagonal(D[0], 1.0 + tau2)
         D[q - 1] = sig2 * np.eye(k)
         e = np.exp(-s)
@@ -130,6 +147,12 @@ class CovarianceFamily:
             else:
                 D[1] = sum(per_axis[:-1])
                 D[2] = per_axis[-1]
+        elif self.kernel_code == KERNEL_MATERN:
+            from scipy.special import gammaln, kv
+            with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+                drho = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + (nu + 1.0) * np.log(s)) * kv(nu - 1.0, s) / rho[0]
+            D[1] = sig2 * np.where(s < 1e-60, 0.0, drho)
+            D[2] = sig2 * (_matern_corr(nu + MATERN_H, s) - _matern_corr(nu - MATERN_H, s)) / (2.0 * MATERN_H)
         elif self.kernel_code == KERNEL_MATERN15:
             D[1] = sig2 * s * s * e / rho[0]
         elif self.kernel_code == KERNEL_MATERN25:
@@ -146,7 +169,7 @@ class CovarianceFamily:
         a = self.prepare_locs(np.atleast_2d(locs_a))
         b = self.prepare_locs(np.atleast_2d(locs_b))
         s, _ = _scaled_distance(a, b, _axis_ranges(self.name, theta, a.shape[1]))
-        return theta[0] * _correlation(self.kernel_code, s)
+        return theta[0] * _correlation(self.kernel_code, s, theta[2] if self.kernel_code == KERNEL_MATERN else None)
 
 
 _REGISTRY = {name: CovarianceFamily(name, code) for name, code in _CODES.items()}

@@ -13,7 +13,20 @@
 #define VB_MAXQ (VB_MAXD + 2) // covariance parameters
 #define VB_MAXP 16            // design columns
 
-enum : int { FAM_EXP_ISO = 0, FAM_EXP_ANISO = 1, FAM_EXP_SPACETIME = 2, FAM_MATERN15 = 3, FAM_MATERN25 = 4 };
+enum : int { FAM_EXP_ISO = 0, FAM_EXP_ANISO = 1, FAM_EXP_SPACETIME = 2, FAM_MATERN15 = 3, FAM_MATERN25 = 4,
+             FAM_MATERN = 5 };
+
+// Order-dependent constants of Temme's method for K_nu (they depend on the smoothness only, so the
+// host computes them once per evaluation): nu = mu + nup with |mu| <= 1/2.
+struct MaternOrder {
+    double nu, mu;
+    double gam1, gam2;   // Temme's Gamma_1(mu), Gamma_2(mu)
+    double gampl, gammi; // 1/Gamma(1+mu), 1/Gamma(1-mu)
+    double fact;         // pi mu / sin(pi mu)
+    double normcon;      // 2^(1-nu) / Gamma(nu)
+    int nup, pad_;
+};
+#define VB_MATERN_H 1e-5 // central-difference step of the smoothness derivative
 
 // Everything one evaluation needs, passed by value as the kernel argument.
 struct EvalParams {
@@ -35,6 +48,7 @@ struct EvalParams {
     int *fail_rows;          // optional (i1-i0) pivot+1 per observation
     int ws_doubles;          // per-warp scratch doubles (warp_smem layout)
     const unsigned int *pair_tab; // tiled layout: off-diagonal pair table of the tier (device memory)
+    MaternOrder mat[3];      // FAM_MATERN only: orders nu, nu + h, nu - h
 };
 
 // ---------------------------------------------------------------------------
@@ -101,13 +115,113 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab)
     return __hiloint2double(__double2hiint(v) + ((ki >> 5) << 20), __double2loint(v));
 }
 
+// K_nu(x) and K_{nu-1}(x), x > 0, by Temme's method (N. M. Temme, J. Comput. Phys. 19 (1975) 324):
+// the series in x for x <= 2, Steed's continued fraction CF2 for x > 2, both for the fractional
+// order mu, then the upward recurrence K_{a+1} = K_{a-1} + (2a/x) K_a.  CUDA has no Bessel K of
+// real order (the reason the paper's package has no general Matern).
+static __device__ __noinline__ void bessel_k_pair(double x, const MaternOrder &M, double &knu, double &knum1)
+{
+    const double mu = M.mu;
+    double kmu, kmu1;
+    if (x <= 2.0) {
+        const double xh = 0.5 * x;
+        const double d = -log(xh);
+        double e = mu * d;
+        const double fact2 = (fabs(e) < 1e-10) ? 1.0 : sinh(e) / e;
+        double ff = M.fact * (M.gam1 * cosh(e) + M.gam2 * fact2 * d);
+        double sum = ff;
+        e = exp(e);
+        double p = 0.5 * e / M.gampl, q = 0.5 / (e * M.gammi), c = 1.0, sum1 = p;
+        const double d2 = xh * xh, mu2 = mu * mu;
+        for (int i = 1; i < 400; ++i) {
+            ff = (i * ff + p + q) / (i * i - mu2);
+            c *= d2 / i;
+            p /= (i - mu);
+            q /= (i + mu);
+            const double del = c * ff;
+            sum += del;
+            sum1 += c * (p - i * ff);
+            if (fabs(del) < fabs(sum) * 1e-17)
+                break;
+        }
+        kmu = sum;
+        kmu1 = sum1 / xh;
+    } else {
+        double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+        const double a1 = 0.25 - mu * mu;
+        double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
+        for (int i = 2; i < 400; ++i) {
+            a -= 2 * (i - 1);
+            c = -a * c / i;
+            const double qnew = (q1 - b * q2) / a;
+            q1 = q2;
+            q2 = qnew;
+            q += c * qnew;
+            b += 2.0;
+            d = 1.0 / (b + a * d);
+            delh = (b * d - 1.0) * delh;
+            h += delh;
+            const double dels = q * delh;
+            s += dels;
+            if (fabs(dels) < fabs(s) * 1e-17)
+                break;
+        }
+        kmu = sqrt(1.5707963267948966 / x) * exp(-x) / s;
+        kmu1 = kmu * (mu + x + 0.5 - a1 * h) / x;
+    }
+    if (M.nup == 0) {
+        knu = kmu;
+        knum1 = kmu1 - (2.0 * mu / x) * kmu; // K_{mu-1}
+    } else {
+        double prev = kmu, cur = kmu1;
+        for (int i = 1; i < M.nup; ++i) {
+            const double next = prev + (2.0 * (mu + i) / x) * cur;
+            prev = cur;
+            cur = next;
+        }
+        knu = cur;
+        knum1 = prev;
+    }
+}
+
+// General Matern pair terms at scaled distance x = r/range: correlation 2^(1-nu)/Gamma(nu) x^nu K_nu(x),
+// its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative by a
+// central difference of step VB_MATERN_H (the convention of the oracle; GpGp differentiates the
+// smoothness numerically as well).
+__device__ __forceinline__ void matern_terms(const EvalParams &P, double x, double inv_rho, double &Kv, double &Drange,
+                                             double &Dnu)
+{
+    if (x < 1e-60) { // coincident points: the x -> 0 limits
+        Kv = P.sig2;
+        Drange = 0.0;
+        Dnu = 0.0;
+        return;
+    }
+    const double lx = log(x);
+    double k, km1, kp, km, unused;
+    bessel_k_pair(x, P.mat[0], k, km1);
+    bessel_k_pair(x, P.mat[1], kp, unused);
+    bessel_k_pair(x, P.mat[2], km, unused);
+    const double xn = exp(P.mat[0].nu * lx);
+    Kv = P.sig2 * P.mat[0].normcon * xn * k;
+    Drange = P.sig2 * P.mat[0].normcon * xn * x * km1 * inv_rho;
+    const double cp = P.mat[1].normcon * exp(P.mat[1].nu * lx) * kp;
+    const double cm = P.mat[2].normcon * exp(P.mat[2].nu * lx) * km;
+    Dnu = P.sig2 * (cp - cm) * (0.5 / VB_MATERN_H);
+}
+
 // Covariance and range-derivative values of one off-diagonal pair.
 //   dl[l] = pa[l] - pc[l] is supplied by the caller (coordinates in the working frame).
 // Families follow include/vecchia_b200.h.  Dv has qd entries.
 template <int FAM>
 __device__ __forceinline__ void pair_terms(const EvalParams &P, const double *dl, double &Kv, double *Dv)
 {
-    if (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
+    if (FAM == FAM_MATERN) {
+        double d2 = 0.0;
+        for (int l = 0; l < P.d; ++l)
+            d2 = fma(dl[l], dl[l], d2);
+        matern_terms(P, sqrt(d2) * P.inv_rho[0], P.inv_rho[0], Kv, Dv[0], Dv[1]);
+    } else if (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
         double d2 = 0.0;
         for (int l = 0; l < P.d; ++l)
             d2 = fma(dl[l], dl[l], d2);

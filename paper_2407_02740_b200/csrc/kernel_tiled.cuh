@@ -31,7 +31,7 @@
 
 template <int FAM, int D>
 struct FamTraits {
-    static constexpr int QD = (FAM == FAM_EXP_ANISO) ? D : (FAM == FAM_EXP_SPACETIME ? 2 : 1);
+    static constexpr int QD = (FAM == FAM_EXP_ANISO) ? D : ((FAM == FAM_EXP_SPACETIME || FAM == FAM_MATERN) ? 2 : 1);
     static constexpr int Q = QD + 2;
 };
 
@@ -44,7 +44,13 @@ template <int FAM, int D>
 __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *etab, const double (&dl)[D],
                                              double &Kv, double (&Dv)[FamTraits<FAM, D>::QD])
 {
-    if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
+    if constexpr (FAM == FAM_MATERN) {
+        double x2 = 1e-300;
+#pragma unroll
+        for (int l = 0; l < D; ++l)
+            x2 = fma(dl[l], dl[l], x2);
+        matern_terms(E, x2 * rsqrt_pos(x2), E.inv_rho[0], Kv, Dv[0], Dv[1]);
+    } else if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
         double x2 = 1e-300;
 #pragma unroll
         for (int l = 0; l < D; ++l)

@@ -166,6 +166,8 @@ extern "C" int vb200_family_nparms(int family, int d)
         return d + 2;
     case VB200_EXP_SPACETIME:
         return d >= 2 ? 4 : VB200_EINVAL;
+    case VB200_MATERN:
+        return 4;
     default:
         return VB200_EINVAL;
     }
@@ -339,6 +341,31 @@ extern "C" int vb200_set_layout(vb200_problem *P, int layout)
 // ---------------------------------------------------------------------------
 // evaluation
 // ---------------------------------------------------------------------------
+// Temme constants of one order (host, long double gamma): Gamma_1 = (1/G(1-mu) - 1/G(1+mu)) / (2 mu),
+// Gamma_2 = (1/G(1-mu) + 1/G(1+mu)) / 2; for tiny |mu| the odd part of the reciprocal-gamma Taylor
+// series is used: Gamma_1 -> -(euler_gamma + a3 mu^2), a3 = -0.0420026350340952.
+static MaternOrder matern_order(double nu)
+{
+    MaternOrder M;
+    memset(&M, 0, sizeof(M));
+    M.nu = nu;
+    M.nup = (int)std::floor(nu + 0.5);
+    M.mu = nu - M.nup;
+    const long double mu = (long double)M.mu;
+    const long double gp = 1.0L / tgammal(1.0L + mu), gm = 1.0L / tgammal(1.0L - mu);
+    M.gampl = (double)gp;
+    M.gammi = (double)gm;
+    M.gam2 = (double)(0.5L * (gm + gp));
+    if (fabsl(mu) < 1e-4L)
+        M.gam1 = (double)(-(0.5772156649015328606L - 0.0420026350340952L * mu * mu));
+    else
+        M.gam1 = (double)((gm - gp) / (2.0L * mu));
+    const long double pimu = 3.14159265358979323846264338L * mu;
+    M.fact = (fabsl(pimu) < 1e-9L) ? 1.0 : (double)(pimu / sinl(pimu));
+    M.normcon = std::exp((1.0 - nu) * 0.6931471805599453 - std::lgamma(nu));
+    return M;
+}
+
 static int fill_params(const vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
                        int64_t i1, EvalParams &E)
 {
@@ -396,6 +423,14 @@ static int fill_params(const vb200_problem *P, int family, const double *theta, 
     }
     E.fail_word = P->fail_word;
     E.fail_count = P->fail_count;
+    if (family == VB200_MATERN) {
+        const double nu0 = theta[2];
+        if (!(nu0 > 2.0 * VB_MATERN_H) || nu0 > 60.0)
+            return fail(VB200_EINVAL, "matern_isotropic: smoothness must lie in (2e-5, 60]");
+        const double orders[3] = {nu0, nu0 + VB_MATERN_H, nu0 - VB_MATERN_H};
+        for (int t = 0; t < 3; ++t)
+            E.mat[t] = matern_order(orders[t]);
+    }
     return VB200_OK;
 }
 
@@ -421,6 +456,7 @@ static ws_kernel_t ws_kernel_for(int family)
     case VB200_EXP_ANISO: return vecchia_warp_smem_kernel<FAM_EXP_ANISO>;
     case VB200_EXP_SPACETIME: return vecchia_warp_smem_kernel<FAM_EXP_SPACETIME>;
     case VB200_MATERN15: return vecchia_warp_smem_kernel<FAM_MATERN15>;
+    case VB200_MATERN: return vecchia_warp_smem_kernel<FAM_MATERN>;
     default: return vecchia_warp_smem_kernel<FAM_MATERN25>;
     }
 }
