@@ -46,7 +46,9 @@ def algorithmic_flops(family: str, d: int, p: int, q: int, m: int) -> dict:
     T = k * (k - 1) // 2
     pair = {"exponential_isotropic": 3 * d + 6, "exponential_sphere": 3 * d + 6, "matern15_isotropic": 3 * d + 10,
             "matern25_isotropic": 3 * d + 13, "exponential_spacetime": 4 * d + 11,
-            "exponential_anisotropic": 4 * d + 8 + 3 * d}[family]
+            "exponential_anisotropic": 4 * d + 8 + 3 * d,
+            # general Matern: 3 Bessel evaluations count as 1 "flop" each, like exp (SURVEY 8d convention)
+            "matern_isotropic": 3 * d + 20}[family]
     qd = q - 2
     cov = T * pair + 2 * k
     chol = sum((a + 1) ** 2 for a in range(k))

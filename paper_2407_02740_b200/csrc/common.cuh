@@ -186,7 +186,7 @@ static __device__ __noinline__ void bessel_k_pair(double x, const MaternOrder &M
 
 // General Matern pair terms at scaled distance x = r/range: correlation 2^(1-nu)/Gamma(nu) x^nu K_nu(x),
 // its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative by a
-// central difference of step VB_MATERN_H (the convention of the oracle; GpGp differentiates the
+// central difference of step VB_MATERN_H (part of the family definition here; GpGp differentiates the
 // smoothness numerically as well).
 __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, double inv_rho, double &Kv, double &Drange,
                                              double &Dnu)

@@ -154,6 +154,10 @@ FAMILY_SHAPES = [
     ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 40),
     ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 60),
     ("exponential_isotropic", 2, 3, [1.5, 0.25, 0.1], 15),
+    ("matern_isotropic", 2, 1, [1.0, 0.08, 0.8, 0.1], 30),
+    ("matern_isotropic", 3, 4, [1.0, 0.2, 2.2, 0.05], 30),
+    ("matern_isotropic", 2, 2, [1.2, 0.1, 0.3, 0.1], 12),
+    ("matern_isotropic", 2, 1, [1.2, 0.1, 1.5, 0.1], 45),
 ]
 
 
@@ -183,7 +187,7 @@ def test_every_compiled_tiled_instance_against_oracle():
     narrow one (heavy front padding), plus the ragged head rows, against the CPU oracle."""
     from paper_2407_02740_b200 import _cabi
     names = {0: "exponential_isotropic", 1: "exponential_anisotropic", 2: "exponential_spacetime",
-             3: "matern15_isotropic", 4: "matern25_isotropic"}
+             3: "matern15_isotropic", 4: "matern25_isotropic", 5: "matern_isotropic"}
     inst = _cabi.tiled_instances()
     assert len(inst) >= 60
     rng = np.random.default_rng(77)
@@ -191,6 +195,8 @@ def test_every_compiled_tiled_instance_against_oracle():
         family = names[fam]
         q = _cabi.load().vb200_family_nparms(fam, d)
         theta = np.concatenate([[1.3], rng.uniform(0.15, 0.4, q - 2), [0.08]])
+        if fam == 5:
+            theta[2] = rng.uniform(0.4, 2.6)  # smoothness
         for m in sorted({cap - 2, max(2, cap // 2 - 3)}):
             n = 3 * cap + 40
             y, X, locs, _ = make_instance(1000 + cap + d + p + m, n, d, p)

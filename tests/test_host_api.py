@@ -109,7 +109,7 @@ def test_covariance_registry_known_answers():
 @pytest.mark.parametrize("family,d,theta", [
     ("exponential_isotropic", 2, [1.3, 0.4, 0.2]), ("exponential_anisotropic", 3, [1.3, 0.4, 0.7, 0.2, 0.1]),
     ("exponential_spacetime", 3, [1.3, 0.4, 0.9, 0.1]), ("matern15_isotropic", 2, [0.9, 0.3, 0.05]),
-    ("matern25_isotropic", 2, [0.9, 0.3, 0.05])])
+    ("matern25_isotropic", 2, [0.9, 0.3, 0.05]), ("matern_isotropic", 2, [0.9, 0.3, 1.3, 0.05])])
 def test_covariance_derivatives_vs_finite_differences(family, d, theta):
     from oracle import numpy_families
     rng = np.random.default_rng(1)
@@ -119,7 +119,9 @@ def test_covariance_derivatives_vs_finite_differences(family, d, theta):
     D = fam.derivatives(theta, pts)
     K0, D0 = numpy_families.cov_and_derivs(family, theta, pts)
     np.testing.assert_allclose(fam.matrix(theta, pts), K0, rtol=1e-13)
-    np.testing.assert_allclose(D, D0, rtol=1e-12, atol=1e-14)
+    # the smoothness derivative is a central difference of step 1e-5: rounding differences of the two
+    # distance computations are amplified by 1e5 there
+    np.testing.assert_allclose(D, D0, rtol=1e-8 if family == "matern_isotropic" else 1e-12, atol=1e-14)
     for j in range(theta.shape[0]):
         h = 1e-6 * theta[j]
         tp, tm = theta.copy(), theta.copy()

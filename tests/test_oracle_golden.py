@@ -108,7 +108,37 @@ def test_spacetime_is_constrained_anisotropic():
     np.testing.assert_allclose(s["ainfo"], J.T @ a["ainfo"] @ J, rtol=1e-11)
 
 
-@pytest.mark.parametrize("family", ["matern15_isotropic", "matern25_isotropic", "exponential_spacetime"])
+def test_bessel_k_against_scipy_and_closed_forms():
+    from scipy.special import kv
+    L = vo.lib()
+    for nu in (0.2, 0.5, 0.8, 1.0, 1.5, 2.3, 3.7, 5.0, 0.49999, 0.50001, 1e-3, 12.5):
+        for x in (1e-8, 1e-3, 0.1, 0.5, 1.0, 1.9999, 2.0, 2.0001, 3.0, 10.0, 50.0, 300.0):
+            want = kv(nu, x)
+            if np.isfinite(want) and want > 0:
+                assert L.vo_bessel_k(nu, x) == pytest.approx(want, rel=2e-13), (nu, x)
+    x = 0.7  # K_{1/2}(x) = sqrt(pi/2x) e^-x
+    assert L.vo_bessel_k(0.5, x) == pytest.approx(np.sqrt(np.pi / (2 * x)) * np.exp(-x), rel=1e-14)
+
+
+def test_general_matern_reduces_to_closed_forms():
+    rng = np.random.default_rng(3)
+    n = 80
+    locs = rng.uniform(0, 1, (n, 2)); y = rng.normal(size=n)
+    X = np.column_stack([np.ones(n), rng.normal(size=n)])
+    nn = vo.neighbor_scan(locs, 12)
+    for nu, closed in ((0.5, "exponential_isotropic"), (1.5, "matern15_isotropic"), (2.5, "matern25_isotropic")):
+        g = vo.split_acc(vo.run(y, X, locs, nn, "matern_isotropic", [0.9, 0.15, nu, 0.05]), 2, 4)
+        c = vo.split_acc(vo.run(y, X, locs, nn, closed, [0.9, 0.15, 0.05]), 2, 3)
+        keep = [0, 1, 3]  # variance, range, nugget
+        for k in ("logdet", "ysy", "xsx", "ysx"):
+            np.testing.assert_allclose(g[k], c[k], rtol=1e-11)
+        np.testing.assert_allclose(g["dlogdet"][keep], c["dlogdet"], rtol=1e-9)
+        np.testing.assert_allclose(g["dysy"][keep], c["dysy"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(g["ainfo"][np.ix_(keep, keep)], c["ainfo"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("family", ["matern15_isotropic", "matern25_isotropic", "exponential_spacetime",
+                                    "matern_isotropic"])
 def test_extension_families_structural(family):
     """Families absent from the reference: C oracle == independent numpy oracle,
     derivative fields == central finite differences, dense exactness at m = n-1
@@ -119,6 +149,8 @@ def test_extension_families_structural(family):
     locs = rng.uniform(0, 1, (n, d)); y = rng.normal(size=n)
     X = np.column_stack([np.ones(n), rng.normal(size=n)])
     theta = np.array([1.4, 0.3, 0.5, 0.15]) if d == 3 else np.array([1.4, 0.3, 0.15])
+    if family == "matern_isotropic":
+        theta = np.array([1.4, 0.3, 0.8, 0.15])
     nn = vo.neighbor_scan(locs, m)
     q = theta.shape[0]
     tot = vo.run(y, X, locs, nn, family, theta)
