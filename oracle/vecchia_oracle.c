@@ -635,6 +635,96 @@ int vo_run(const double *y, const double *X, const double *locs, const int64_t *
     return 0;
 }
 
+/*
+ * Nearest-neighbour kriging, restating predict.py:35-90 (krige): for every
+ * prediction point, the m_pred training rows with the smallest (d2, index) in
+ * working coordinates (predict.py:27-32), their joint covariance with the
+ * nugget on the diagonal, the nugget-free cross covariance, a lower Cholesky
+ * factor and two forward solves.  mean_resid = half_k . half_r is the
+ * conditional mean of the residual y - X beta (the caller adds X* beta);
+ * var = prior - half_k . half_k BEFORE the clamp at 0 and the square root.
+ * nbrs (nstar, m_pred) receives the chosen training indices.  Returns 0, or
+ * 1 + the index of the first point whose factorization failed.
+ */
+int64_t vo_krige(const double *y, const double *X, const double *locs, int64_t n, int p, int d,
+                 const double *theta, int q, int family, const double *beta, const double *locs_star,
+                 int64_t nstar, int m_pred, int latent, int workers, double *mean_resid, double *var,
+                 int64_t *nbrs)
+{
+    problem_t P = {y, X, locs, NULL, theta, n, p, d, q, m_pred, family, 0.0};
+    const int k = m_pred;
+    int64_t failed = 0;
+    if (workers < 1)
+        workers = 1;
+    const double prior = latent ? theta[0] : theta[0] * (1.0 + theta[q - 1]);
+#pragma omp parallel num_threads(workers)
+    {
+        double *bd = (double *)malloc(sizeof(double) * (size_t)k);
+        int64_t *bi = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+        double *K = (double *)malloc(sizeof(double) * (size_t)k * k);
+        double *kv = (double *)malloc(sizeof(double) * (size_t)k * 3);
+        double *hk = kv + k, *hr = kv + 2 * k;
+#pragma omp for schedule(static)
+        for (int64_t t = 0; t < nstar; ++t) {
+            const double *xs = locs_star + t * d;
+            int nb = 0;
+            for (int64_t j = 0; j < n; ++j) {
+                double d2 = 0.0;
+                for (int l = 0; l < d; ++l) {
+                    double diff = locs[j * d + l] - xs[l];
+                    d2 += diff * diff;
+                }
+                if (nb == k && d2 >= bd[k - 1])
+                    continue;
+                if (nb < k)
+                    ++nb;
+                int pos = nb - 1;
+                while (pos > 0 && bd[pos - 1] > d2) {
+                    bd[pos] = bd[pos - 1];
+                    bi[pos] = bi[pos - 1];
+                    --pos;
+                }
+                bd[pos] = d2;
+                bi[pos] = j;
+            }
+            for (int a = 0; a < k; ++a) {
+                if (nbrs)
+                    nbrs[t * k + a] = bi[a];
+                for (int b = 0; b < a; ++b)
+                    K[a * k + b] = pair_cov(&P, locs + bi[a] * d, locs + bi[b] * d, 0);
+                K[a * k + a] = pair_cov(&P, locs + bi[a] * d, locs + bi[a] * d, 1);
+                kv[a] = pair_cov(&P, locs + bi[a] * d, xs, 0);
+            }
+            if (factor_lower(K, k, k)) {
+#pragma omp critical
+                if (!failed || t + 1 < failed)
+                    failed = t + 1;
+                continue;
+            }
+            solve_forward(K, k, k, kv, 1, hk, 1);
+            for (int a = 0; a < k; ++a) {
+                double r = y[bi[a]];
+                for (int b = 0; b < p; ++b)
+                    r -= X[bi[a] * p + b] * beta[b];
+                kv[a] = r;
+            }
+            solve_forward(K, k, k, kv, 1, hr, 1);
+            double m0 = 0.0, v0 = 0.0;
+            for (int a = 0; a < k; ++a) {
+                m0 += hk[a] * hr[a];
+                v0 += hk[a] * hk[a];
+            }
+            mean_resid[t] = m0;
+            var[t] = prior - v0;
+        }
+        free(bd);
+        free(bi);
+        free(K);
+        free(kv);
+    }
+    return failed;
+}
+
 /* exhaustive ordered nearest-predecessor scan; out is (n, m+1), pre-filled -1 */
 void vo_neighbor_scan(const double *locs, int64_t n, int d, int m, int workers, int64_t *out)
 {

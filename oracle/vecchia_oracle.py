@@ -61,6 +61,10 @@ def lib():
             _c_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_int64,
             ctypes.c_int, _c_dp, _c_i32p,
         ]
+        L.vo_krige.restype = ctypes.c_int64
+        L.vo_krige.argtypes = [_c_dp, _c_dp, _c_dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _c_dp, ctypes.c_int,
+                               ctypes.c_int, _c_dp, _c_dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               _c_dp, _c_dp, _c_i64p]
         L.vo_bessel_k.restype = ctypes.c_double
         L.vo_bessel_k.argtypes = [ctypes.c_double, ctypes.c_double]
         L.vo_neighbor_scan.restype = None
@@ -165,6 +169,26 @@ def neighbor_scan(locs, m, workers=None):
     lib().vo_neighbor_scan(_dp(locs), n, d, m, int(workers or os.cpu_count() or 1),
                            out.ctypes.data_as(_c_i64p))
     return out
+
+
+def krige(y, X, locs, family, theta, beta, locs_star, X_star, m_pred, latent=False, workers=None):
+    """Kriging mean / sd at locs_star (working coordinates) -- restates the reference's predict.krige
+    (predict.py:35-90).  Returns (mean, sd, neighbor indices)."""
+    y, X, locs, _, theta = _prep(y, X, locs, np.zeros((1, 1), dtype=np.int64), theta)
+    beta = np.ascontiguousarray(beta, dtype=np.float64).ravel()
+    locs_star = np.ascontiguousarray(np.atleast_2d(locs_star), dtype=np.float64)
+    X_star = np.ascontiguousarray(np.atleast_2d(X_star), dtype=np.float64)
+    n, p, d, q, ns = y.shape[0], X.shape[1], locs.shape[1], theta.shape[0], locs_star.shape[0]
+    mean = np.zeros(ns)
+    var = np.zeros(ns)
+    nbrs = np.zeros((ns, m_pred), dtype=np.int64)
+    code = FAMILY_CODES[family] if isinstance(family, str) else int(family)
+    bad = lib().vo_krige(_dp(y), _dp(X), _dp(locs), n, p, d, _dp(theta), q, code, _dp(beta), _dp(locs_star), ns,
+                         int(m_pred), int(bool(latent)), int(workers or os.cpu_count() or 1), _dp(mean), _dp(var),
+                         nbrs.ctypes.data_as(_c_i64p))
+    if bad:
+        raise OracleNotPositiveDefinite(-1, bad - 1)
+    return X_star @ beta + mean, np.sqrt(np.maximum(var, 0.0)), nbrs
 
 
 LOG_2PI = float(np.log(2.0 * np.pi))

@@ -19,6 +19,7 @@ Files written
   neighbors.npz      ordered-neighbor tables incl. exact-tie grids
   fit_cases.npz      full Fisher-scoring fits (theta_hat, trace, iterations, ...)
   config1.npz        BASELINE config 1 (n=10 000, m=30): y + reference results
+  krige_cases.npz    nearest-neighbour kriging (predict.krige) means / sds, noisy and latent
 """
 from __future__ import annotations
 
@@ -236,9 +237,49 @@ def config1():
     print("config1: loglik", res.loglik, "iters", res.iterations, "theta", res.theta_hat.theta)
 
 
+def krige_cases():
+    """Nearest-neighbour kriging outputs of the unmodified reference (predict.py:35-90)."""
+    from vecchiagp.model import FitResult
+    from vecchiagp.predict import krige
+    out = {}
+    specs = [("iso_m10", 31, 300, 2, 2, "exponential_isotropic", [1.5, 0.25, 0.1], 10, 40),
+             ("iso_m60", 32, 400, 2, 1, "exponential_isotropic", [2.0, 0.2, 0.1], 60, 50),
+             ("aniso_m20", 33, 250, 3, 2, "exponential_anisotropic", [1.2, 0.3, 0.2, 0.4, 0.15], 20, 30),
+             ("sphere_m15", 34, 200, 2, 1, "exponential_sphere", [1.5, 0.3, 0.1], 15, 25),
+             ("iso_all", 35, 30, 2, 1, "exponential_isotropic", [1.0, 0.4, 0.05], 30, 10)]
+    for name, seed, n, d, p, family, theta, m_pred, npred in specs:
+        ds, cov = make_instance(seed, n, d, p, family, theta)
+        rng = np.random.default_rng(seed + 100)
+        if family == "exponential_sphere":
+            star = np.column_stack([rng.uniform(-180, 180, npred), np.degrees(np.arcsin(rng.uniform(-1, 1, npred)))])
+        else:
+            star = rng.uniform(0.0, 1.0, (npred, d))
+        star[0] = ds.locs[5]  # one prediction point coincides with a training point
+        Xs = np.ones((npred, p))
+        if p > 1:
+            Xs[:, 1:] = rng.normal(size=(npred, p - 1))
+        beta = rng.normal(size=p)
+        fr = FitResult(theta_hat=cov, beta_hat=beta, beta_cov=np.eye(p), loglik_trace=[0.0], fisher_info=np.eye(3),
+                       iterations=0, converged=True)
+        out[f"{name}/y"], out[f"{name}/X"], out[f"{name}/locs"] = ds.y, ds.X, ds.locs
+        out[f"{name}/theta"], out[f"{name}/family"], out[f"{name}/beta"] = cov.theta, np.array(family), beta
+        out[f"{name}/locs_star"], out[f"{name}/X_star"], out[f"{name}/m_pred"] = star, Xs, np.array(m_pred)
+        for latent in (False, True):
+            ps = krige(fr, ds, star, Xs, m_pred=m_pred, latent=latent, with_sd=True)
+            out[f"{name}/mean_latent{int(latent)}"] = ps.mean
+            out[f"{name}/sd_latent{int(latent)}"] = ps.sd
+    out["names"] = np.array([s[0] for s in specs])
+    np.savez_compressed(OUT / "krige_cases.npz", **out)
+    print("krige_cases.npz:", len(specs), "cases")
+
+
 if __name__ == "__main__":
+    if "--krige-only" in sys.argv:
+        krige_cases()
+        sys.exit(0)
     engine_cases()
     failure_cases()
     neighbor_cases()
     fit_cases()
     config1()
+    krige_cases()
