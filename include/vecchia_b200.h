@@ -145,6 +145,23 @@ int vb200_fail_info(vb200_problem *prob, int64_t *first_fail, int32_t *pivot);
 int vb200_eval_rows(vb200_problem *prob, int family, const double *theta, int q, double jitter,
                     int64_t i0, int64_t i1, double *rows_host, int32_t *fail_host);
 
+/* ---- kriging ------------------------------------------ */
+/*
+ * Nearest-neighbour kriging at `npred` new points from the training data held by `prob`; replaces
+ * the per-point loop of the reference's predict.krige (predict.py:77-89).  locs_star (npred, d) are
+ * WORKING coordinates, nn_star (npred, m_pred) int64 training indices (any order; -1 pads the tail) --
+ * both host or device pointers.  beta (p) are the mean parameters: the kernel forms the residuals
+ * y - X beta itself.  Outputs (host, npred each): mean_resid = conditional mean of the residual at the
+ * point (the caller adds x*' beta), var = prior - k*' K^-1 k* with prior = variance (latent != 0) or
+ * variance*(1+nugget); var is NOT clamped (the reference clamps at 0 before the square root,
+ * predict.py:88).  *first_fail = lowest point index whose neighbour covariance failed to factor
+ * (the reference raises NotPositiveDefinite(pivot=-1), predict.py:82-85), else -1.
+ * Kernels exist for d in {2,3} and m_pred <= 62; otherwise VB200_EUNSUPPORTED.
+ */
+int vb200_krige(vb200_problem *prob, int family, const double *theta, int q, const double *beta,
+                const double *locs_star, const int64_t *nn_star, int64_t npred, int m_pred, int latent,
+                double *mean_resid, double *var, int64_t *first_fail);
+
 /* number of kernel launches the last vb200_eval* call enqueued, and the name of the
  * main kernel variant (for bench.py's gpu_launches / roofline bookkeeping) */
 int vb200_last_launch_count(const vb200_problem *prob);

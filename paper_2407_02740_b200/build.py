@@ -50,7 +50,8 @@ def build_cuda(force: bool = False, verbose: bool = False, jobs: int | None = No
     from concurrent.futures import ThreadPoolExecutor
 
     headers = sorted(CSRC.glob("*.cuh")) + sorted((CSRC / "gen").glob("*.inc")) + [ROOT / "include" / "vecchia_b200.h"]
-    units = [CSRC / "vecchia_b200.cu"] + sorted((CSRC / "gen").glob("tiled_part_*.cu"))
+    units = ([CSRC / "vecchia_b200.cu"] + sorted((CSRC / "gen").glob("tiled_part_*.cu"))
+             + sorted((CSRC / "gen").glob("krige_part_*.cu")))
     if not force and _newer(CUDA_LIB, headers + units):
         return CUDA_LIB
     LIBDIR.mkdir(exist_ok=True)

@@ -199,6 +199,60 @@ void grid_row(const Grid &G, const Level &L, const double *locs, int d, int64_t 
     }
 }
 
+// ring search around an arbitrary query point (all points of the level are candidates).  The squared
+// distance is evaluated as (train - query), matching the reference's `work_train - point`.
+void grid_query(const Grid &G, const Level &L, const double *locs, int d, const double *xq, Best &B)
+{
+    int cq[3];
+    cell_of(L, G, xq, cq);
+    // distance by which the query lies outside the box along each gridded axis (0 inside)
+    double out2 = 0.0;
+    for (int a = 0; a < L.g; ++a) {
+        const double below = G.lo[a] - xq[a], above = xq[a] - (G.lo[a] + G.ext[a]);
+        const double o = below > 0.0 ? below : (above > 0.0 ? above : 0.0);
+        out2 = o > out2 ? o : out2;
+    }
+    (void)out2;
+    int maxr = 0;
+    for (int a = 0; a < L.g; ++a)
+        maxr = std::max(maxr, std::max(cq[a], L.dims[a] - 1 - cq[a]));
+    for (int r = 0; r <= maxr; ++r) {
+        if (r >= 2 && B.cnt == B.m) {
+            const double lb = (double)(r - 1) * L.h * 0.999999;
+            if (B.worst() < lb * lb)
+                break;
+        }
+        const int z0 = L.g > 2 ? std::max(cq[2] - r, 0) : 0, z1 = L.g > 2 ? std::min(cq[2] + r, L.dims[2] - 1) : 0;
+        const int y0 = L.g > 1 ? std::max(cq[1] - r, 0) : 0, y1 = L.g > 1 ? std::min(cq[1] + r, L.dims[1] - 1) : 0;
+        const int x0 = std::max(cq[0] - r, 0), x1 = std::min(cq[0] + r, L.dims[0] - 1);
+        for (int z = z0; z <= z1; ++z) {
+            const bool zface = L.g > 2 && (z == cq[2] - r || z == cq[2] + r);
+            for (int y = y0; y <= y1; ++y) {
+                const bool yface = L.g > 1 && (y == cq[1] - r || y == cq[1] + r);
+                const int64_t rowbase = ((int64_t)z * L.dims[1] + y) * L.dims[0];
+                if (zface || yface) {
+                    const int64_t s = L.start[rowbase + x0], e = L.start[rowbase + x1 + 1];
+                    for (int64_t t = s; t < e; ++t) {
+                        const int64_t j = L.items[t];
+                        B.offer(sqdist(locs + j * d, xq, d), j);
+                    }
+                } else {
+                    for (int side = 0; side < 2; ++side) {
+                        const int x = side ? cq[0] + r : cq[0] - r;
+                        if (x < 0 || x >= L.dims[0] || (side && r == 0))
+                            continue;
+                        const int64_t s = L.start[rowbase + x], e = L.start[rowbase + x + 1];
+                        for (int64_t t = s; t < e; ++t) {
+                            const int64_t j = L.items[t];
+                            B.offer(sqdist(locs + j * d, xq, d), j);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 } // namespace
 
 extern "C" {
@@ -294,6 +348,56 @@ int vbh_neighbors_grid_rows(const double *locs, int64_t n, int d, int m, int wor
             row[0] = i;
             for (int t = 0; t < m; ++t)
                 row[1 + t] = t < B.cnt ? B.v[t].j : -1;
+        }
+    }
+    return 0;
+}
+
+// m nearest TRAINING points (no ordering constraint) of each query point, ranked by (d2, index)
+// -- the selection rule of the reference's kriging (predict.py:27-32, np.lexsort((index, d2))).
+// out is (nq, m) int64.  Same grid machinery: one level holding all n points.
+int vbh_neighbors_query(const double *locs, int64_t n, int d, const double *queries, int64_t nq, int m, int workers,
+                        int64_t *out)
+{
+    if (!locs || !queries || !out || n < 1 || d < 1 || m < 1 || m > n || nq < 0)
+        return -1;
+    if (n > (int64_t)0x7fffffff)
+        return -2;
+    if (workers < 1)
+        workers = 1;
+    Grid G;
+    G.g = d < 3 ? d : 3;
+    for (int a = 0; a < G.g; ++a) {
+        double lo = locs[a], hi = locs[a];
+        for (int64_t i = 1; i < n; ++i) {
+            const double v = locs[i * d + a];
+            lo = v < lo ? v : lo;
+            hi = v > hi ? v : hi;
+        }
+        G.lo[a] = lo;
+        G.ext[a] = hi - lo;
+    }
+    const bool use_grid = n > 2048;
+    Level L;
+    if (use_grid)
+        build_level(L, G, locs, d, n, std::max(3.0, 0.35 * m));
+#pragma omp parallel num_threads(workers)
+    {
+        std::vector<Cand> buf((size_t)m);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t t = 0; t < nq; ++t) {
+            Best B{buf.data(), m, 0};
+            const double *xq = queries + t * d;
+            if (!use_grid) {
+                for (int64_t j = 0; j < n; ++j)
+                    B.offer(sqdist(locs + j * d, xq, d), j);
+            } else {
+                // a query outside the bounding box is clamped into the border cell; its true distance to
+                // any cell is then larger than the in-grid bound used by the stopping rule (conservative)
+                grid_query(G, L, locs, d, xq, B);
+            }
+            for (int k = 0; k < m; ++k)
+                out[t * m + k] = k < B.cnt ? B.v[k].j : -1;
         }
     }
     return 0;

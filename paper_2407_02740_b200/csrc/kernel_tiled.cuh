@@ -40,7 +40,7 @@ struct FamTraits {
 // squared norm is x^2 = (r/rho)^2 directly.  Squared norms start from 1e-300 instead of 0:
 // coincident points then give x ~ 1e-150, i.e. exactly the reference's values (exp(-0) = 1, zero
 // range derivative) without a special case.
-template <int FAM, int D>
+template <int FAM, int D, bool DERIV = true>
 __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *etab, const double (&dl)[D],
                                              double &Kv, double (&Dv)[FamTraits<FAM, D>::QD])
 {
@@ -49,7 +49,18 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
 #pragma unroll
         for (int l = 0; l < D; ++l)
             x2 = fma(dl[l], dl[l], x2);
-        matern_terms(E, x2 * rsqrt_pos(x2), E.inv_rho[0], Kv, Dv[0], Dv[1]);
+        if constexpr (DERIV) {
+            matern_terms(E, x2 * rsqrt_pos(x2), E.inv_rho[0], Kv, Dv[0], Dv[1]);
+        } else { // covariance only (kriging): one Bessel evaluation instead of three
+            const double x = x2 * rsqrt_pos(x2);
+            double k, km1;
+            Kv = E.sig2;
+            if (x >= 1e-60) {
+                bessel_k_pair(x, E.mat[0], k, km1);
+                Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * log(x)) * k;
+            }
+            Dv[0] = Dv[1] = 0.0;
+        }
     } else if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
         double x2 = 1e-300;
 #pragma unroll

@@ -746,6 +746,91 @@ extern "C" int vb200_last_kernel_ms(vb200_problem *P, double *ms)
     return VB200_OK;
 }
 
+extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, int q, const double *beta,
+                           const double *locs_star, const int64_t *nn_star, int64_t npred, int m_pred, int latent,
+                           double *mean_resid, double *var, int64_t *first_fail)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    if (!beta || !locs_star || !nn_star || !mean_resid || !var)
+        return fail(VB200_EINVAL, "NULL argument");
+    if (npred < 0 || m_pred < 1 || m_pred > P->n)
+        return fail(VB200_EINVAL, "m_pred must be in [1, n]");
+    CUDA_TRY(cudaSetDevice(P->device));
+    EvalParams E;
+    int rc = fill_params(P, family, theta, q, 0.0, P->nn_row0, P->nn_row0, E);
+    if (rc)
+        return rc;
+    if (first_fail)
+        *first_fail = -1;
+    if (npred == 0)
+        return VB200_OK;
+    const KrigeInstance *inst = krige_find(family, m_pred, P->d);
+    if (!inst)
+        return fail(VB200_EUNSUPPORTED, "no kriging kernel for this family / dimension / m_pred (d in {2,3}, m_pred <= 62)");
+    E.pair_tab = tiled_pair_table(inst->g, inst->s);
+    if (!E.pair_tab)
+        return fail(VB200_ECUDA, "pair table allocation failed");
+    KrigeParams K;
+    memset(&K, 0, sizeof(K));
+    K.npred = npred;
+    K.m_pred = m_pred;
+    K.prior = latent ? theta[0] : theta[0] * (1.0 + theta[q - 1]);
+    for (int b = 0; b < P->p; ++b)
+        K.beta[b] = beta[b];
+    double *d_locs = nullptr, *d_out = nullptr;
+    int64_t *d_nn = nullptr;
+    const size_t lbytes = sizeof(double) * (size_t)npred * P->d, nbytes = sizeof(int64_t) * (size_t)npred * m_pred;
+    if (is_device_ptr(locs_star)) {
+        K.locs_star = locs_star;
+    } else {
+        CUDA_TRY(cudaMallocAsync(&d_locs, lbytes, P->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_locs, locs_star, lbytes, cudaMemcpyHostToDevice, P->stream));
+        K.locs_star = d_locs;
+    }
+    if (is_device_ptr(nn_star)) {
+        K.nn_star = nn_star;
+    } else {
+        CUDA_TRY(cudaMallocAsync(&d_nn, nbytes, P->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_nn, nn_star, nbytes, cudaMemcpyHostToDevice, P->stream));
+        K.nn_star = d_nn;
+    }
+    CUDA_TRY(cudaMallocAsync(&d_out, sizeof(double) * 2 * (size_t)npred, P->stream));
+    K.mean_resid = d_out;
+    K.var = d_out + npred;
+    reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
+    const size_t smem = (size_t)inst->smem_doubles * sizeof(double);
+    if (smem > P->smem_optin)
+        return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
+    CUDA_TRY(cudaFuncSetAttribute(inst->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaFuncSetAttribute(inst->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inst->kernel, 32, smem));
+    if (per_sm < 1)
+        per_sm = 1;
+    const int opw = 32 / inst->g;
+    const int64_t nbatch = (npred + opw - 1) / opw;
+    int64_t blocks = (int64_t)P->sm_count * per_sm;
+    if (blocks > nbatch)
+        blocks = nbatch;
+    inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+    CUDA_TRY(cudaGetLastError());
+    P->last_kernel = inst->name;
+    P->last_launches = 2;
+    if (int rc0 = ensure_host_fail(P))
+        return rc0;
+    CUDA_TRY(cudaMemcpyAsync(mean_resid, d_out, sizeof(double) * (size_t)npred, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(var, d_out + npred, sizeof(double) * (size_t)npred, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream));
+    if (d_locs) cudaFreeAsync(d_locs, P->stream);
+    if (d_nn) cudaFreeAsync(d_nn, P->stream);
+    cudaFreeAsync(d_out, P->stream);
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    if (*P->h_fail != ~0ull && first_fail)
+        *first_fail = (int64_t)(*P->h_fail >> 16);
+    return VB200_OK;
+}
+
 extern "C" int vb200_last_launch_count(const vb200_problem *P) { return P ? P->last_launches : 0; }
 extern "C" const char *vb200_last_kernel_name(const vb200_problem *P) { return P ? P->last_kernel : ""; }
 

@@ -121,6 +121,9 @@ def host_library():
         lib.vbh_neighbors_grid_rows.restype = ctypes.c_int
         lib.vbh_neighbors_grid_rows.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                 ctypes.c_int64, ctypes.c_int64, ip]
+        lib.vbh_neighbors_query.restype = ctypes.c_int
+        lib.vbh_neighbors_query.argtypes = [dp, ctypes.c_int64, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int,
+                                            ctypes.c_int, ip]
         lib.vbh_max_threads.restype = ctypes.c_int
         _host = lib
     return _host
@@ -177,4 +180,23 @@ def find_ordered_neighbor_rows(locs, m: int, row0: int, rows: int, workers: int 
         out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     if rc != 0:
         raise RuntimeError(f"neighbor search failed with code {rc}")
+    return out
+
+
+def find_nearest_training(work_train, work_star, m_pred: int, workers: int | None = None) -> np.ndarray:
+    """(nstar, m_pred) int64 indices of the m_pred training rows nearest to each query point, ranked by
+    (squared distance, index) -- the selection of the reference's kriging (predict.py:27-32)."""
+    a = np.ascontiguousarray(np.atleast_2d(work_train), dtype=np.float64)
+    b = np.ascontiguousarray(np.atleast_2d(work_star), dtype=np.float64)
+    if a.shape[1] != b.shape[1]:
+        raise ValueError("training and prediction coordinates differ in dimension")
+    if not 1 <= m_pred <= a.shape[0]:
+        raise ValueError(f"m_pred must be in [1, n]={a.shape[0]}, got {m_pred}")
+    out = np.full((b.shape[0], m_pred), SENTINEL, dtype=np.int64)
+    rc = host_library().vbh_neighbors_query(
+        a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.shape[0], a.shape[1],
+        b.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), b.shape[0], int(m_pred), _worker_count(workers),
+        out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    if rc != 0:
+        raise RuntimeError(f"neighbor query failed with code {rc}")
     return out

@@ -39,6 +39,11 @@ def neighbor_cases():
 
 
 @pytest.fixture(scope="session")
+def krige_cases():
+    return np.load(GOLDEN / "krige_cases.npz")
+
+
+@pytest.fixture(scope="session")
 def config1_golden():
     return np.load(GOLDEN / "config1.npz")
 

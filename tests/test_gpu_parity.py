@@ -310,3 +310,50 @@ def test_full_size_properties_n2_20():
         k = 1 << 14
         want = vo.run(y, X, locs, nn.idx, "matern15_isotropic", theta, i0=0, i1=k)
         fields_close(prob.totals(theta, i0=0, i1=k), want, 1, 3, 1e-9)
+
+
+# ---- kriging: reference predict.krige ------------------------------------------
+@pytest.mark.parametrize("name", ["iso_m10", "iso_m60", "aniso_m20", "sphere_m15", "iso_all"])
+def test_kriging_matches_reference(krige_cases, name):
+    z = krige_cases
+    g = lambda k: z[f"{name}/{k}"]
+    train = vg.Dataset(g("y"), g("X"), g("locs"))
+    cov = vg.CovarianceParameters(str(g("family")), g("theta"))
+    p = train.p
+    fr = vg.FitResult(theta_hat=cov, beta_hat=g("beta"), beta_cov=np.eye(p), loglik_trace=[0.0],
+                      fisher_info=np.eye(cov.nparms), iterations=0, converged=True)
+    for latent in (False, True):
+        ps = vg.krige(fr, train, g("locs_star"), g("X_star"), m_pred=int(g("m_pred")), latent=latent)
+        want_m, want_s = g(f"mean_latent{int(latent)}"), g(f"sd_latent{int(latent)}")
+        assert np.max(np.abs(ps.mean - want_m)) <= 1e-9 * max(1.0, np.max(np.abs(want_m)))
+        # sd = sqrt(prior - k'K^-1 k): at a prediction point on top of a training point with latent=True
+        # the variance is a cancellation to ~0, so compare variances on the prior's scale
+        prior = cov.theta[0] * (1.0 if latent else 1.0 + cov.theta[-1])
+        assert np.max(np.abs(ps.sd ** 2 - want_s ** 2)) <= 1e-9 * prior
+    no_sd = vg.krige(fr, train, g("locs_star"), g("X_star"), m_pred=int(g("m_pred")), with_sd=False)
+    assert no_sd.sd is None
+    with pytest.raises(vg.LengthMismatch):
+        vg.krige(fr, train, g("locs_star"), g("X_star")[:-1], m_pred=int(g("m_pred")))
+    with pytest.raises(ValueError):
+        vg.krige(fr, train, g("locs_star"), g("X_star"), m_pred=train.n + 1)
+
+
+@pytest.mark.parametrize("family,d,theta", [("matern15_isotropic", 2, [1.2, 0.1, 0.1]),
+                                            ("matern_isotropic", 3, [1.0, 0.2, 0.8, 0.05]),
+                                            ("exponential_spacetime", 3, [1.3, 0.2, 0.5, 0.1]),
+                                            ("matern25_isotropic", 3, [0.8, 0.15, 0.02])])
+def test_kriging_extension_families_against_oracle(family, d, theta):
+    rng = np.random.default_rng(8)
+    n, npred, m_pred = 6000, 500, 30
+    y, X, locs, theta = make_instance(321, n, d, 2, family, theta)
+    star = rng.uniform(0, 1, (npred, d))
+    Xs = np.column_stack([np.ones(npred), rng.normal(size=npred)])
+    beta = np.array([0.3, -0.7])
+    cov = vg.CovarianceParameters(family, theta)
+    fr = vg.FitResult(theta_hat=cov, beta_hat=beta, beta_cov=np.eye(2), loglik_trace=[0.0],
+                      fisher_info=np.eye(cov.nparms), iterations=0, converged=True)
+    ps = vg.krige(fr, vg.Dataset(y, X, locs), star, Xs, m_pred=m_pred)
+    mean, sd, _ = vo.krige(y, X, locs, family, theta, beta, star, Xs, m_pred)
+    np.testing.assert_allclose(ps.mean, mean, rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(ps.sd ** 2, sd ** 2, rtol=1e-9, atol=1e-12)
+    assert vg.rmse(ps.mean, mean) < 1e-9

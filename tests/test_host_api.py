@@ -174,6 +174,28 @@ def test_neighbor_grid_equals_exhaustive_scan_with_ties_and_row_ranges():
     assert vg.find_ordered_neighbors(np.zeros((1, 2)), 5).idx.shape == (1, 2)
 
 
+def test_nearest_training_query_equals_exhaustive_ranking():
+    from paper_2407_02740_b200.preprocess import find_nearest_training
+    rng = np.random.default_rng(5)
+    for n, d, m, nq in [(5000, 2, 60, 200), (3000, 3, 20, 150), (900, 2, 10, 60), (4000, 1, 5, 80)]:
+        train = rng.uniform(0, 1, (n, d))
+        qs = rng.uniform(-0.3, 1.3, (nq, d))   # some queries outside the bounding box
+        qs[0] = train[7]                         # a query on top of a training point
+        got = find_nearest_training(train, qs, m, workers=3)
+        for t in range(0, nq, 7):
+            diff = train - qs[t]
+            d2 = (diff * diff).sum(axis=1)
+            want = np.lexsort((np.arange(n), d2))[:m]   # the reference's rule, predict.py:27-32
+            assert np.array_equal(got[t], want)
+    g = np.stack(np.meshgrid(np.arange(60.0), np.arange(60.0)), -1).reshape(-1, 2)
+    got = find_nearest_training(g, g[::11], 12)          # exact ties on an integer grid
+    for t, qpt in enumerate(g[::11]):
+        d2 = ((g - qpt) ** 2).sum(axis=1)
+        assert np.array_equal(got[t], np.lexsort((np.arange(len(g)), d2))[:12])
+    with pytest.raises(ValueError):
+        find_nearest_training(g, g[:2], 0)
+
+
 # ---- inference -----------------------------------------------------------------
 def test_fisher_step_known_answers():
     # reference tests/test_inference.py:84-115

@@ -170,3 +170,24 @@ def test_extension_families_structural(family):
     Ki = np.linalg.inv(K)
     info = np.array([[0.5 * np.trace(Ki @ D[j] @ Ki @ D[l]) for l in range(q)] for j in range(q)])
     np.testing.assert_allclose(ev["info"], info, rtol=1e-7)
+
+
+KRIGE = ["iso_m10", "iso_m60", "aniso_m20", "sphere_m15", "iso_all"]
+
+
+@pytest.mark.parametrize("name", KRIGE)
+def test_kriging_oracle_matches_reference(krige_cases, name):
+    """oracle vo_krige == the unmodified reference's predict.krige (LAPACK Cholesky there, own here)."""
+    import paper_2407_02740_b200 as vg
+    z = krige_cases
+    g = lambda k: z[f"{name}/{k}"]
+    fam = vg.covariance_registry(str(g("family")))
+    work, ws = fam.prepare_locs(g("locs")), fam.prepare_locs(g("locs_star"))
+    for latent in (0, 1):
+        mean, sd, nbrs = vo.krige(g("y"), g("X"), work, str(g("family")), g("theta"), g("beta"), ws, g("X_star"),
+                                  int(g("m_pred")), latent=latent)
+        np.testing.assert_allclose(mean, g(f"mean_latent{latent}"), rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(sd, g(f"sd_latent{latent}"), rtol=1e-10, atol=1e-12)
+    # the host neighbour query of the product selects the same rows in the same order
+    from paper_2407_02740_b200.preprocess import find_nearest_training
+    assert np.array_equal(find_nearest_training(work, ws, int(g("m_pred"))), nbrs)
