@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <vector>
 #ifdef _OPENMP
 #include <omp.h>
@@ -399,6 +400,129 @@ int vbh_neighbors_query(const double *locs, int64_t n, int d, const double *quer
             for (int k = 0; k < m; ++k)
                 out[t * m + k] = k < B.cnt ? B.v[k].j : -1;
         }
+    }
+    return 0;
+}
+
+// Max-min distance ordering (BASELINE.json config 1 names it, the reference has
+// only identity / random orderings).  Definition: perm[0] = the point nearest the coordinate-wise
+// mean (smallest index on ties); perm[k] = the not-yet-chosen point whose minimum distance to
+// {perm[0..k-1]} is largest (smallest index on ties).  Exact greedy selection in ~O(n log n): every
+// point keeps its current min squared distance d[j]; a lazy max-heap yields the next point i*, and
+// only points within sqrt(d[i*]) of i* can have their d[j] lowered (all d[j] <= d[i*]), which a
+// uniform grid enumerates.  out receives the permutation (new position -> original index).
+int vbh_order_maxmin(const double *locs, int64_t n, int d, int64_t *out)
+{
+    if (!locs || !out || n < 1 || d < 1)
+        return -1;
+    if (n > (int64_t)0x7fffffff)
+        return -2;
+    for (int64_t t = 0; t < n * d; ++t)
+        if (!std::isfinite(locs[t]))
+            return -3;
+    // first point: nearest to the centroid
+    std::vector<double> mean((size_t)d, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int l = 0; l < d; ++l)
+            mean[l] += locs[i * d + l];
+    for (int l = 0; l < d; ++l)
+        mean[l] /= (double)n;
+    int64_t first = 0;
+    double best = sqdist(locs, mean.data(), d);
+    for (int64_t i = 1; i < n; ++i) {
+        const double v = sqdist(locs + i * d, mean.data(), d);
+        if (v < best) {
+            best = v;
+            first = i;
+        }
+    }
+    Grid G;
+    G.g = d < 3 ? d : 3;
+    for (int a = 0; a < G.g; ++a) {
+        double lo = locs[a], hi = locs[a];
+        for (int64_t i = 1; i < n; ++i) {
+            const double v = locs[i * d + a];
+            lo = v < lo ? v : lo;
+            hi = v > hi ? v : hi;
+        }
+        G.lo[a] = lo;
+        G.ext[a] = hi - lo;
+    }
+    Level L;
+    build_level(L, G, locs, d, n, 3.0);
+    std::vector<int64_t> fill(L.start.begin() + 1, L.start.end()); // live end of every cell (swap-remove)
+    std::vector<int32_t> slot((size_t)n);                          // position of a point inside items
+    for (int64_t c = 0; c + 1 < (int64_t)L.start.size(); ++c)
+        for (int64_t t = L.start[c]; t < L.start[c + 1]; ++t)
+            slot[L.items[t]] = (int32_t)t;
+    auto remove_point = [&](int64_t i) {
+        int c[3];
+        cell_of(L, G, locs + i * d, c);
+        const int64_t cell = ((int64_t)c[2] * L.dims[1] + c[1]) * L.dims[0] + c[0];
+        const int64_t pos = slot[i], last = --fill[cell];
+        const int32_t moved = L.items[last];
+        L.items[pos] = moved;
+        slot[moved] = (int32_t)pos;
+        L.items[last] = (int32_t)i;
+    };
+    std::vector<double> dmin((size_t)n);
+    typedef std::pair<double, int64_t> Key; // (d, -index): max-heap pops the largest d, smallest index on ties
+    std::vector<Key> heap;
+    heap.reserve((size_t)n * 2);
+    for (int64_t i = 0; i < n; ++i) {
+        dmin[i] = sqdist(locs + i * d, locs + first * d, d);
+        if (i != first)
+            heap.emplace_back(dmin[i], -i);
+    }
+    std::make_heap(heap.begin(), heap.end());
+    std::vector<char> chosen((size_t)n, 0);
+    chosen[first] = 1;
+    remove_point(first);
+    out[0] = first;
+    for (int64_t k = 1; k < n; ++k) {
+        int64_t pick = -1;
+        double r2 = 0.0;
+        while (!heap.empty()) {
+            std::pop_heap(heap.begin(), heap.end());
+            const Key top = heap.back();
+            heap.pop_back();
+            const int64_t i = -top.second;
+            if (!chosen[i] && top.first == dmin[i]) {
+                pick = i;
+                r2 = top.first;
+                break;
+            }
+        }
+        if (pick < 0)
+            return -4;
+        out[k] = pick;
+        chosen[pick] = 1;
+        remove_point(pick);
+        // lower d[j] of the live points within sqrt(r2) of the pick
+        const double *xp = locs + pick * d;
+        const double r = std::sqrt(r2) * 1.000001 + 1e-300;
+        int c0[3] = {0, 0, 0}, c1[3] = {0, 0, 0};
+        for (int a = 0; a < L.g; ++a) {
+            int lo = (int)std::floor((xp[a] - r - G.lo[a]) * L.inv_h), hi = (int)std::floor((xp[a] + r - G.lo[a]) * L.inv_h);
+            c0[a] = lo < 0 ? 0 : (lo >= L.dims[a] ? L.dims[a] - 1 : lo);
+            c1[a] = hi < 0 ? 0 : (hi >= L.dims[a] ? L.dims[a] - 1 : hi);
+        }
+        for (int z = c0[2]; z <= c1[2]; ++z)
+            for (int y = c0[1]; y <= c1[1]; ++y) {
+                const int64_t rowbase = ((int64_t)z * L.dims[1] + y) * L.dims[0];
+                for (int x = c0[0]; x <= c1[0]; ++x) {
+                    const int64_t cell = rowbase + x;
+                    for (int64_t t = L.start[cell]; t < fill[cell]; ++t) {
+                        const int64_t j = L.items[t];
+                        const double v = sqdist(locs + j * d, xp, d);
+                        if (v < dmin[j]) {
+                            dmin[j] = v;
+                            heap.emplace_back(v, -j);
+                            std::push_heap(heap.begin(), heap.end());
+                        }
+                    }
+                }
+            }
     }
     return 0;
 }

@@ -49,6 +49,23 @@ def random_permutation(n: int, seed: int) -> Ordering:
     return Ordering(gen.permutation(n).astype(np.int64))
 
 
+def maxmin_ordering(locs) -> Ordering:
+    """Max-min distance ordering of working coordinates (an addition: the reference offers identity and
+    random orderings only, model.py:135-136; BASELINE.json config 1 names maxmin).  Position 0 is the
+    point nearest the centroid; each following point maximises its minimum distance to all earlier
+    ones (smallest index on ties).  Exact greedy selection, ~O(n log n) (csrc/host_neighbors.cpp)."""
+    locs = np.ascontiguousarray(np.atleast_2d(locs), dtype=np.float64)
+    out = np.empty(locs.shape[0], dtype=np.int64)
+    rc = host_library().vbh_order_maxmin(locs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), locs.shape[0],
+                                         locs.shape[1], out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    if rc == -3:
+        from .errors import NonFiniteValue
+        raise NonFiniteValue("non-finite coordinate in locs")
+    if rc != 0:
+        raise RuntimeError(f"maxmin ordering failed with code {rc}")
+    return Ordering(out)
+
+
 def reorder_dataset(ds: Dataset, ordering: Ordering) -> Dataset:
     if ordering.n != ds.n:
         raise LengthMismatch(f"permutation length {ordering.n} does not match n={ds.n}")
@@ -124,6 +141,8 @@ def host_library():
         lib.vbh_neighbors_query.restype = ctypes.c_int
         lib.vbh_neighbors_query.argtypes = [dp, ctypes.c_int64, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int,
                                             ctypes.c_int, ip]
+        lib.vbh_order_maxmin.restype = ctypes.c_int
+        lib.vbh_order_maxmin.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ip]
         lib.vbh_max_threads.restype = ctypes.c_int
         _host = lib
     return _host

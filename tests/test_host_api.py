@@ -196,6 +196,29 @@ def test_nearest_training_query_equals_exhaustive_ranking():
         find_nearest_training(g, g[:2], 0)
 
 
+def test_maxmin_ordering_equals_brute_force_greedy():
+    def brute(locs):
+        n = len(locs)
+        first = int(np.argmin(((locs - locs.mean(axis=0)) ** 2).sum(1)))
+        perm, dmin = [first], ((locs - locs[first]) ** 2).sum(1)
+        dmin[first] = -1.0
+        for _ in range(1, n):
+            i = int(np.argmax(dmin))          # smallest index on ties
+            perm.append(i)
+            dmin = np.minimum(dmin, ((locs - locs[i]) ** 2).sum(1))
+            dmin[perm] = -1.0
+        return np.array(perm)
+
+    rng = np.random.default_rng(0)
+    for n, d in [(700, 2), (500, 3), (300, 1), (400, 4)]:
+        locs = rng.uniform(0, 1, (n, d))
+        assert np.array_equal(vg.maxmin_ordering(locs).perm, brute(locs))
+    grid = np.stack(np.meshgrid(np.arange(15.0), np.arange(15.0)), -1).reshape(-1, 2)   # exact ties
+    assert np.array_equal(vg.maxmin_ordering(grid).perm, brute(grid))
+    assert vg.maxmin_ordering(np.zeros((1, 2))).perm.tolist() == [0]
+    assert vg.ModelSpec(vg.CovarianceParameters("exponential_isotropic", [1, 1, 0]), m=5, ordering="maxmin").m == 5
+
+
 # ---- inference -----------------------------------------------------------------
 def test_fisher_step_known_answers():
     # reference tests/test_inference.py:84-115
