@@ -216,10 +216,17 @@ def ours_arm(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise vg.DeviceUnavailable("bench.py needs a CUDA device: the cuda core has no CPU fallback")
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    # one rank per GPU; VB200_BENCH_BACKEND=gloo lets several ranks share one GPU (used only to
+    # exercise the sharded code path on a single-GPU box -- never for reported numbers)
+    backend = os.environ.get("VB200_BENCH_BACKEND", "nccl")
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     n_total = world * args.n
@@ -262,7 +269,7 @@ def ours_arm(args):
     kernel_ms = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev_index) as clocks:
         start.record()
         for _ in range(args.steps):
             totals = step(prob)
@@ -315,7 +322,7 @@ def ours_arm(args):
     # ---- roofline of the main kernel (FP64 DFMA bound; measured peak) ----
     burst, sustained = np.zeros(1), np.zeros(1)
     dp = lambda a: a.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_double))
-    _cabi.check(_cabi.load().vb200_measure_fp64_peak(local_rank, 0.5, dp(burst), dp(sustained)), "fp64 peak")
+    _cabi.check(_cabi.load().vb200_measure_fp64_peak(dev_index, 0.5, dp(burst), dp(sustained)), "fp64 peak")
     F = algorithmic_flops(args.family, args.d, args.p, q, args.m)
     k_ms = float(np.mean(kernel_ms))
     achieved = F["F_min"] * (i1 - i0) / (k_ms * 1e-3) * 1e-12
@@ -405,7 +412,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=1 << 20, help="observations per GPU")
+    ap.add_argument("--n-per-gpu", dest="n", type=int, default=1 << 20, help="observations per GPU")
     ap.add_argument("--m", type=int, default=30)
     ap.add_argument("--d", type=int, default=2)
     ap.add_argument("--p", type=int, default=1)

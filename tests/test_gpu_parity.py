@@ -357,3 +357,61 @@ def test_kriging_extension_families_against_oracle(family, d, theta):
     np.testing.assert_allclose(ps.mean, mean, rtol=1e-9, atol=1e-9)
     np.testing.assert_allclose(ps.sd ** 2, sd ** 2, rtol=1e-9, atol=1e-12)
     assert vg.rmse(ps.mean, mean) < 1e-9
+
+
+# ---- sharded (multi-rank) evaluation on the device: two ranks share this GPU, gloo all-reduce ------
+_SHARD_WORKER = r"""
+import os, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+import paper_2407_02740_b200 as vg
+from paper_2407_02740_b200 import distributed, engine
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(0)
+rng = np.random.default_rng(3)
+n, m = 20000, 30
+locs = rng.uniform(0, 1, (n, 2)); y = rng.normal(size=n) + np.sin(5 * locs[:, 0]); X = np.ones((n, 1))
+ds = vg.Dataset(y, X, locs)
+nn = vg.find_ordered_neighbors(locs, m)
+theta = np.array([1.2, 0.1, 0.2])
+ev = distributed.ShardedEvaluator(ds, nn, "matern15_isotropic")
+assert (ev.i0, ev.i1) == distributed.shard_bounds(n, world, rank)
+sharded = ev.totals(theta)
+with engine.DeviceProblem(ds, nn, "matern15_isotropic") as whole:
+    single = whole.totals(theta)
+scale = np.maximum(np.abs(single), 1e-300)
+assert np.max(np.abs(sharded - single) / scale) < 1e-12, np.max(np.abs(sharded - single) / scale)
+# the same Fisher-scoring fit from the sharded evaluator and from the single-GPU engine
+start = vg.default_start(ds, "matern15_isotropic")
+a = vg.fit(ds, nn, vg.ModelSpec(covariance=start, m=m), evaluator=ev)
+b = vg.fit(ds, nn, vg.ModelSpec(covariance=start, m=m))
+assert np.allclose(a.theta_hat.theta, b.theta_hat.theta, rtol=1e-9), (a.theta_hat.theta, b.theta_hat.theta)
+assert a.iterations == b.iterations
+# a failure on one shard is reported by every rank with the globally lowest index
+locs2 = locs.copy(); locs2[15000] = locs2[14990]
+nn2 = vg.find_ordered_neighbors(locs2, m)
+ev2 = distributed.ShardedEvaluator(vg.Dataset(y, X, locs2), nn2, "exponential_isotropic")
+try:
+    ev2.totals(np.array([1.0, 0.3, 0.0]))
+    raise SystemExit("expected NotPositiveDefinite")
+except vg.NotPositiveDefinite as err:
+    assert err.observation == 15000, err.observation
+ev.close(); ev2.close()
+dist.destroy_process_group()
+print("rank", rank, "ok")
+"""
+
+
+def test_sharded_evaluator_two_ranks_one_gpu(tmp_path):
+    import os, subprocess, sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    script = tmp_path / "shard_worker.py"
+    script.write_text(_SHARD_WORKER.format(root=root))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29577", WORLD_SIZE="2")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-3000:]
