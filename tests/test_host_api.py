@@ -219,6 +219,26 @@ def test_maxmin_ordering_equals_brute_force_greedy():
     assert vg.ModelSpec(vg.CovarianceParameters("exponential_isotropic", [1, 1, 0]), m=5, ordering="maxmin").m == 5
 
 
+def test_binary_formats_round_trip(tmp_path):
+    from paper_2407_02740_b200 import io
+    rng = np.random.default_rng(2)
+    ds = vg.Dataset(rng.normal(size=50), rng.normal(size=(50, 2)), rng.uniform(size=(50, 3)))
+    nn = vg.find_ordered_neighbors(ds.locs, 6)
+    io.write_dataset_npz(ds, tmp_path / "d.npz")
+    io.write_neighbors_npy(nn, tmp_path / "nn.npy")
+    back = io.read_dataset_npz(tmp_path / "d.npz")
+    assert np.array_equal(back.y, ds.y) and np.array_equal(back.X, ds.X) and np.array_equal(back.locs, ds.locs)
+    assert np.array_equal(io.read_neighbors_npy(tmp_path / "nn.npy").idx, nn.idx)
+    assert np.array_equal(io.read_neighbors_npy(tmp_path / "nn.npy", mmap=True).idx[10:20], nn.idx[10:20])
+    fit = vg.FitResult(vg.CovarianceParameters("matern15_isotropic", [1.0, 0.1 + 1e-17, 0.3]), np.array([0.5, 1.0]),
+                       np.eye(2), [-3.0, -2.5], np.eye(3), 4, True, {"fit_ms": 1.5})
+    io.write_fit_json(fit, tmp_path / "f.json", config={"m": 6})
+    doc = io.read_fit_json(tmp_path / "f.json")
+    assert tuple(doc) == io.FIT_SCHEMA_KEYS          # the reference's schema, key for key (io.py:128-140)
+    again = io.fit_from_dict(doc)
+    assert np.array_equal(again.theta_hat.theta, fit.theta_hat.theta) and again.loglik == -2.5 and again.converged
+
+
 # ---- inference -----------------------------------------------------------------
 def test_fisher_step_known_answers():
     # reference tests/test_inference.py:84-115
