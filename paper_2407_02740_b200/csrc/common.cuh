@@ -16,6 +16,9 @@
 enum : int { FAM_EXP_ISO = 0, FAM_EXP_ANISO = 1, FAM_EXP_SPACETIME = 2, FAM_MATERN15 = 3, FAM_MATERN25 = 4,
              FAM_MATERN = 5 };
 
+#define VB_MATERN_TERMS 12 // series terms (x <= 2: (x/2)^(2i)/(i!)^2 < 1e-17 at i = 12)
+#define VB_MATERN_CF 48    // tabulated continued-fraction iterations (beyond: plain divisions)
+
 // Order-dependent constants of Temme's method for K_nu (they depend on the smoothness only, so the
 // host computes them once per evaluation): nu = mu + nup with |mu| <= 1/2.
 struct MaternOrder {
@@ -25,6 +28,13 @@ struct MaternOrder {
     double fact;         // pi mu / sin(pi mu)
     double normcon;      // 2^(1-nu) / Gamma(nu)
     int nup, pad_;
+    double inv_mu;       // 1/mu (0 when mu == 0; only used for |mu d| >= 1e-2)
+    // reciprocals that depend on (iteration, mu) only -- the divisions of Temme's series and of
+    // Steed's continued fraction become multiplications by kernel-parameter (constant-bank) values
+    double r1[VB_MATERN_TERMS]; // 1 / (i^2 - mu^2), i = 1..
+    double rp[VB_MATERN_TERMS]; // 1 / (i - mu)
+    double rq[VB_MATERN_TERMS]; // 1 / (i + mu)
+    double ra[VB_MATERN_CF];    // 1 / a_i of CF2, a_i = mu^2 - 1/4 - i(i-1), i = 2..
 };
 #define VB_MATERN_H 1e-5 // central-difference step of the smoothness derivative
 
@@ -119,63 +129,67 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab)
 // the series in x for x <= 2, Steed's continued fraction CF2 for x > 2, both for the fractional
 // order mu, then the upward recurrence K_{a+1} = K_{a-1} + (2a/x) K_a.  CUDA has no Bessel K of
 // real order (the reason the paper's package has no general Matern).
-static __device__ __noinline__ void bessel_k_pair(double x, const MaternOrder &M, double &knu, double &knum1)
+// `d` = -log(x/2) and `inv_x` = 1/x are shared by the three orders evaluated per pair.
+static __device__ __noinline__ void bessel_k_pair(double x, double d, double inv_x, const MaternOrder &M, double &knu,
+                                                  double &knum1)
 {
     const double mu = M.mu;
     double kmu, kmu1;
     if (x <= 2.0) {
         const double xh = 0.5 * x;
-        const double d = -log(xh);
-        double e = mu * d;
-        const double fact2 = (fabs(e) < 1e-10) ? 1.0 : sinh(e) / e;
-        double ff = M.fact * (M.gam1 * cosh(e) + M.gam2 * fact2 * d);
+        const double e = mu * d;
+        const double E = exp(e), Ei = rcp_pos(E);
+        const double e2 = e * e;
+        // sinh(e)/e: series for small e, (E - 1/E) / (2e) otherwise
+        const double shoe = (fabs(e) < 1e-2) ? fma(e2, fma(e2, 1.0 / 120.0, 1.0 / 6.0), 1.0)
+                                             : 0.5 * (E - Ei) * M.inv_mu * rcp_pos(d);
+        double ff = M.fact * fma(M.gam1, 0.5 * (E + Ei), M.gam2 * shoe * d);
         double sum = ff;
-        e = exp(e);
-        double p = 0.5 * e / M.gampl, q = 0.5 / (e * M.gammi), c = 1.0, sum1 = p;
-        const double d2 = xh * xh, mu2 = mu * mu;
-        for (int i = 1; i < 400; ++i) {
-            ff = (i * ff + p + q) / (i * i - mu2);
-            c *= d2 / i;
-            p /= (i - mu);
-            q /= (i + mu);
-            const double del = c * ff;
-            sum += del;
-            sum1 += c * (p - i * ff);
-            if (fabs(del) < fabs(sum) * 1e-17)
-                break;
+        double p = 0.5 * E * rcp_pos(M.gampl), q = 0.5 * Ei * rcp_pos(M.gammi), c = 1.0, sum1 = p;
+        const double d2 = xh * xh;
+#pragma unroll
+        for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
+            ff = fma((double)i, ff, p + q) * M.r1[i - 1];
+            c *= d2 * (1.0 / i);
+            p *= M.rp[i - 1];
+            q *= M.rq[i - 1];
+            sum = fma(c, ff, sum);
+            sum1 = fma(c, fma(-(double)i, ff, p), sum1);
         }
         kmu = sum;
-        kmu1 = sum1 / xh;
+        kmu1 = sum1 * (2.0 * inv_x);
     } else {
-        double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+        double b = 2.0 * (1.0 + x), dd = rcp_pos(b), h = dd, delh = dd, q1 = 0.0, q2 = 1.0;
         const double a1 = 0.25 - mu * mu;
-        double q = a1, c = a1, a = -a1, s = 1.0 + q * delh;
+        double q = a1, c = a1, a = -a1, s = fma(q, delh, 1.0);
         for (int i = 2; i < 400; ++i) {
             a -= 2 * (i - 1);
+            const bool tab = (i - 2) < VB_MATERN_CF;
+            const double inv_a = tab ? M.ra[tab ? i - 2 : 0] : 1.0 / a;
             c = -a * c / i;
-            const double qnew = (q1 - b * q2) / a;
+            const double qnew = (q1 - b * q2) * inv_a;
             q1 = q2;
             q2 = qnew;
-            q += c * qnew;
+            q = fma(c, qnew, q);
             b += 2.0;
-            d = 1.0 / (b + a * d);
-            delh = (b * d - 1.0) * delh;
+            dd = rcp_pos(fma(a, dd, b));
+            delh = fma(b, dd, -1.0) * delh;
             h += delh;
             const double dels = q * delh;
             s += dels;
             if (fabs(dels) < fabs(s) * 1e-17)
                 break;
         }
-        kmu = sqrt(1.5707963267948966 / x) * exp(-x) / s;
-        kmu1 = kmu * (mu + x + 0.5 - a1 * h) / x;
+        kmu = sqrt(1.5707963267948966 * inv_x) * exp(-x) / s;
+        kmu1 = kmu * (mu + x + 0.5 - a1 * h) * inv_x;
     }
     if (M.nup == 0) {
         knu = kmu;
-        knum1 = kmu1 - (2.0 * mu / x) * kmu; // K_{mu-1}
+        knum1 = fma(-2.0 * mu * inv_x, kmu, kmu1); // K_{mu-1}
     } else {
         double prev = kmu, cur = kmu1;
         for (int i = 1; i < M.nup; ++i) {
-            const double next = prev + (2.0 * (mu + i) / x) * cur;
+            const double next = fma(2.0 * (mu + i) * inv_x, cur, prev);
             prev = cur;
             cur = next;
         }
@@ -198,10 +212,11 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
         return;
     }
     const double lx = log(x);
+    const double d = 0.6931471805599453 - lx, inv_x = rcp_pos(x); // -log(x/2), 1/x: shared by the three orders
     double k, km1, kp, km, unused;
-    bessel_k_pair(x, P.mat[0], k, km1);
-    bessel_k_pair(x, P.mat[1], kp, unused);
-    bessel_k_pair(x, P.mat[2], km, unused);
+    bessel_k_pair(x, d, inv_x, P.mat[0], k, km1);
+    bessel_k_pair(x, d, inv_x, P.mat[1], kp, unused);
+    bessel_k_pair(x, d, inv_x, P.mat[2], km, unused);
     const double xn = exp(P.mat[0].nu * lx);
     Kv = P.sig2 * P.mat[0].normcon * xn * k;
     Drange = P.sig2 * P.mat[0].normcon * xn * x * km1 * inv_rho;

@@ -56,8 +56,9 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
             double k, km1;
             Kv = E.sig2;
             if (x >= 1e-60) {
-                bessel_k_pair(x, E.mat[0], k, km1);
-                Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * log(x)) * k;
+                const double lx = log(x);
+                bessel_k_pair(x, 0.6931471805599453 - lx, rcp_pos(x), E.mat[0], k, km1);
+                Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * lx) * k;
             }
             Dv[0] = Dv[1] = 0.0;
         }

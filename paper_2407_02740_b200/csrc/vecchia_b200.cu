@@ -363,6 +363,17 @@ static MaternOrder matern_order(double nu)
     const long double pimu = 3.14159265358979323846264338L * mu;
     M.fact = (fabsl(pimu) < 1e-9L) ? 1.0 : (double)(pimu / sinl(pimu));
     M.normcon = std::exp((1.0 - nu) * 0.6931471805599453 - std::lgamma(nu));
+    M.inv_mu = M.mu != 0.0 ? 1.0 / M.mu : 0.0;
+    for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
+        M.r1[i - 1] = (double)(1.0L / ((long double)i * i - mu * mu));
+        M.rp[i - 1] = (double)(1.0L / ((long double)i - mu));
+        M.rq[i - 1] = (double)(1.0L / ((long double)i + mu));
+    }
+    long double a = -(0.25L - mu * mu);
+    for (int i = 2; i < 2 + VB_MATERN_CF; ++i) {
+        a -= 2.0L * (i - 1);
+        M.ra[i - 2] = (double)(1.0L / a);
+    }
     return M;
 }
 
