@@ -62,6 +62,7 @@ def build_cuda(force: bool = False, verbose: bool = False, jobs: int | None = No
              "-I", str(ROOT / "include")]
     if verbose:
         flags.append("-Xptxas=-v")
+    flags += os.environ.get("VB200_NVCC_FLAGS", "").split()  # development knob (e.g. -DTILED_WPB=2)
 
     def compile_one(src: Path) -> Path:
         obj = objdir / (src.stem + ".o")

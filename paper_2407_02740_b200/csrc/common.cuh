@@ -58,6 +58,7 @@ struct EvalParams {
     int *fail_rows;          // optional (i1-i0) pivot+1 per observation
     int ws_doubles;          // per-warp scratch doubles (warp_smem layout)
     const unsigned int *pair_tab; // tiled layout: off-diagonal pair table of the tier (device memory)
+    int sm_count;            // SMs of the device (tiled layout: start stagger of the resident blocks)
     MaternOrder mat[3];      // FAM_MATERN only: orders nu, nu + h, nu - h
 };
 
@@ -89,6 +90,16 @@ __device__ __forceinline__ double rcp_pos(double a)
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
     r = fma(fma(-a, r, 1.0), r, r);
     return fma(fma(-a, r, 1.0), r, r);
+}
+
+// 1/a for positive normal a: MUFU.RCP64H seed (~2^-22 relative) + ONE third-order step
+// r (1 + e + e^2), e = 1 - a r: three dependent DFMA instead of four (it sits on the pivot chain)
+__device__ __forceinline__ double rcp_pos3(double a)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    const double e = fma(-a, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
 // sqrt(a): a * rsqrt(a) with one Newton correction of the product (correctly rounded in practice)
@@ -211,6 +222,12 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
         Dnu = 0.0;
         return;
     }
+    if (x > 705.0) { // x^nu K_nu(x) ~ e^-x underflows (also the far-away padding points of kernel_tiled.cuh,
+        Kv = 0.0;    // for which the continued fraction below would overflow and never converge)
+        Drange = 0.0;
+        Dnu = 0.0;
+        return;
+    }
     const double lx = log(x);
     const double d = 0.6931471805599453 - lx, inv_x = rcp_pos(x); // -log(x/2), 1/x: shared by the three orders
     double k, km1, kp, km, unused;
@@ -223,6 +240,14 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
     const double cp = P.mat[1].normcon * exp(P.mat[1].nu * lx) * kp;
     const double cm = P.mat[2].normcon * exp(P.mat[2].nu * lx) * km;
     Dnu = P.sig2 * (cp - cm) * (0.5 / VB_MATERN_H);
+}
+
+// Out-of-line entry for the fully unrolled row-owner pair phase of kernel_tiled.cuh (keeps ~60 copies of
+// the series / continued-fraction code out of the instruction stream).
+static __device__ __noinline__ void matern_terms_call(const EvalParams &P, double x, double &Kv, double &Drange,
+                                                      double &Dnu)
+{
+    matern_terms(P, x, P.inv_rho[0], Kv, Drange, Dnu);
 }
 
 // Covariance and range-derivative values of one off-diagonal pair.

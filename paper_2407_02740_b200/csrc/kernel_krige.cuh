@@ -11,7 +11,7 @@
 // side and nothing else.  Same lane-group / register layout as kernel_tiled.cuh (G lanes per point,
 // S rows per lane, local row 0 always padding: serves m_pred + 1 <= CAP - 1).
 #pragma once
-#include "kernel_tiled.cuh"
+#include "tiled_common.cuh"
 
 struct KrigeParams {
     const double *locs_star;  // (npred, d) working coordinates of the prediction points

@@ -1,47 +1,58 @@
-// kernel_tiled.cuh -- layout TILED_REG: the fast path.
+// kernel_tiled.cuh -- layout TILED_REG: the fast path of the likelihood evaluation.
 //
-// G lanes of a warp cooperate on one observation (32/G observations per warp).  Every
-// lane owns S rows of the local (CAP x CAP, CAP = G*S) covariance matrix, folded
-// boustrophedon-wise (slot s even: row s*G + lane, slot s odd: row s*G + G-1-lane) so
-// that the triangular work is balanced, and keeps those rows IN REGISTERS for the whole
-// factorization.  Shared memory is used only as a staging / broadcast medium:
-//   * the pair terms (one exp + one sqrt per pair) are computed pair-parallel, perfectly
-//     balanced over the lanes, staged in a packed triangle, then read back row-wise;
-//   * at Cholesky step j the scaled column j is written once and read back as broadcast
-//     128-bit loads (1 LDS per 2 values instead of 4 SHFL); the columns stay in shared
-//     memory and serve the transposed back-substitution for u = B^-T e_last;
-//   * the packed range-derivative matrices D_j wait there for the symmetric mat-vec D_j u.
-// The forward substitutions of y and X ride along inside the Cholesky sweep (their
-// updates use the freshly scaled column that is already in registers).
+// G lanes of a warp cooperate on one observation (32/G observations per warp).  Every lane owns S
+// rows of the local (CAP x CAP, CAP = G*S) covariance matrix, folded boustrophedon-wise (slot s even:
+// row s*G + lane, slot s odd: row s*G + G-1-lane) so that the triangular work is balanced, and keeps
+// those rows IN REGISTERS from the moment their entries are computed until the last sweep.
 //
-// Rows with fewer than CAP live points (the ragged head rows i < m, or m+1 < CAP) are
-// padded at the FRONT of the local frame with identity rows and zero data, which leaves
-// every accumulator term of the real block unchanged (chol([[I,0],[0,K]]) = [[I,0],[0,B]]).
+// The kernel is bound by the shared-memory / shuffle data pipe (LSU), not by FP64 issue (measured:
+// tools/micro/lds_groups.cu -- a broadcast LDS.128 costs 2.2 LSU cycles per warp whatever the number
+// of lane groups, a 32-bit SHFL 1.1, 32 distinct doubles 2), so the design minimises LSU traffic per
+// observation:
+//   * ROW-OWNER pair terms: the lane that owns rows a0 (slot 2h) and a1 (slot 2h+1) evaluates all
+//     pairs (a1, c), c < a1, then (a0, c), c < a0 -- a0 + a1 is the same for every lane, so the pair
+//     work is balanced with NO pair table and NO staging of K: the covariance goes straight into the
+//     register that the factorization will use (static register index: the loop is fully unrolled),
+//     the point of row a is already in registers and the point of column c is one (mostly broadcast)
+//     128-bit load.  Only the range-derivative values go to shared memory (packed triangle D_r).
+//   * at factorization step j the unscaled column j is written once and read back as broadcast
+//     128-bit loads; the columns stay in shared memory and serve the transposed back-substitution
+//     for u = B^-T e_last, into which the symmetric mat-vec D_r u is fused.
+// The forward substitutions of y and X ride along inside the factorization sweep.
 //
-// Same per-observation mathematics as kernel_warp_smem.cuh / the reference's
-// _obs_kernel (/root/reference/pkg/src/vecchiagp/engine/_kernels.pyx:347-381); see
-// common.cuh for the reference map.
+// Rows with fewer than CAP live points (local row 0 always; the ragged head rows i < m; m+1 < CAP-1)
+// are padding rows at the FRONT of the local frame: unit diagonal, zero data, and coordinates 1e30
+// scaled units away from everything (distinct per row), so every pair term that touches them
+// underflows to (at most) 1e-200 without any mask in the pair loop; chol([[I,0],[0,K]]) =
+// [[I,0],[0,B]] leaves every accumulator term of the real block unchanged.
+//
+// Same per-observation mathematics as kernel_warp_smem.cuh / the reference's _obs_kernel
+// (/root/reference/pkg/src/vecchiagp/engine/_kernels.pyx:347-381); see common.cuh for the map.
 #pragma once
-#include "common.cuh"
+#include "tiled_common.cuh"
+#include <type_traits>
 
-#define FULLMASK 0xffffffffu
-#ifndef TILED_NI
-#define TILED_NI 2 // independent pairs in flight per lane in the pair loop (3 and 4 measured no faster)
+#ifndef TILED_WPB
+#define TILED_WPB 1 // warps per block; > 1: the warps of a block pass the phases of a batch together (barriers)
+#endif
+#ifndef TILED_ABLATE
+#define TILED_ABLATE 0 // timing experiments only: bit 0 skips the pair phase, 1 factorization, 2 back-substitution, 3 sweeps, 4 gather loads
+#endif
+#ifndef TILED_PD
+#define TILED_PD 3 // broadcast loads in flight ahead of their FMAs in the factorization
+#endif
+#ifndef TILED_STAGGER_NS
+#define TILED_STAGGER_NS 0 // experiment: start offset between the resident blocks of an SM (measured: no effect)
+#endif
+#ifndef TILED_RNI
+#define TILED_RNI 4 // independent pair evaluations in flight per lane (row-owner pair phase)
 #endif
 
+// exp table premultiplied by sigma^2 (every family's covariance is sigma^2 * exp(-.) * polynomial)
+// and range-derivative values WITHOUT their constant factor (1/range, 1/(3 range), 1/range_axis):
+// the factor is applied once per row to D_r u after the back-substitution (dscale below).
 template <int FAM, int D>
-struct FamTraits {
-    static constexpr int QD = (FAM == FAM_EXP_ANISO) ? D : ((FAM == FAM_EXP_SPACETIME || FAM == FAM_MATERN) ? 2 : 1);
-    static constexpr int Q = QD + 2;
-};
-
-// Pair terms with a compile-time coordinate count.  dl[] are coordinate differences ALREADY
-// divided by the range of their axis (the gather scales the coordinates once per point), so the
-// squared norm is x^2 = (r/rho)^2 directly.  Squared norms start from 1e-300 instead of 0:
-// coincident points then give x ~ 1e-150, i.e. exactly the reference's values (exp(-0) = 1, zero
-// range derivative) without a special case.
-template <int FAM, int D, bool DERIV = true>
-__device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *etab, const double (&dl)[D],
+__device__ __forceinline__ void pair_terms_r(const EvalParams &E, const double *etab, const double (&dl)[D],
                                              double &Kv, double (&Dv)[FamTraits<FAM, D>::QD])
 {
     if constexpr (FAM == FAM_MATERN) {
@@ -49,37 +60,28 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
 #pragma unroll
         for (int l = 0; l < D; ++l)
             x2 = fma(dl[l], dl[l], x2);
-        if constexpr (DERIV) {
-            matern_terms(E, x2 * rsqrt_pos(x2), E.inv_rho[0], Kv, Dv[0], Dv[1]);
-        } else { // covariance only (kriging): one Bessel evaluation instead of three
-            const double x = x2 * rsqrt_pos(x2);
-            double k, km1;
-            Kv = E.sig2;
-            if (x >= 1e-60) {
-                const double lx = log(x);
-                bessel_k_pair(x, 0.6931471805599453 - lx, rcp_pos(x), E.mat[0], k, km1);
-                Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * lx) * k;
-            }
-            Dv[0] = Dv[1] = 0.0;
-        }
+        matern_terms_call(E, x2 * rsqrt_pos(x2), Kv, Dv[0], Dv[1]);
     } else if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
         double x2 = 1e-300;
 #pragma unroll
         for (int l = 0; l < D; ++l)
             x2 = fma(dl[l], dl[l], x2);
-        const double x = x2 * rsqrt_pos(x2);
-        const double se = E.sig2 * exp_neg(x, etab);
-        const double xi = x * E.inv_rho[0];
+        // x = sqrt(x2) = g (1 + e/2 + 3 e^2/8), g = x2 y, e = 1 - x2 y^2, y = MUFU.RSQ64H seed
+        const double y = rsqrt_seed(x2);
+        const double e = fma(-x2, y * y, 1.0);
+        const double g = x2 * y;
+        const double x = fma(fma(e, 0.375, 0.5), g * e, g);
+        const double se = exp_neg(x, etab); // sigma^2 exp(-x)
         if constexpr (FAM == FAM_EXP_ISO) {
             Kv = se;
-            Dv[0] = se * xi;
+            Dv[0] = se * x;                 // * 1/range
         } else if constexpr (FAM == FAM_MATERN15) {
             Kv = fma(se, x, se);
-            Dv[0] = (se * x) * xi;
+            Dv[0] = se * x2;                // * 1/range
         } else {
             const double x1 = 1.0 + x;
-            Kv = se * fma(x * x, 1.0 / 3.0, x1);
-            Dv[0] = (se * x) * (xi * x1) * (1.0 / 3.0);
+            Kv = se * fma(x2, 1.0 / 3.0, x1);
+            Dv[0] = (se * x2) * x1;         // * 1/(3 range)
         }
     } else {
         double sc[D];
@@ -92,67 +94,123 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
                 sp2 += sc[l];
         }
         const double rs = rsqrt_pos(s2);
-        Kv = E.sig2 * exp_neg(s2 * rs, etab);
+        Kv = exp_neg(s2 * rs, etab);
         const double g = Kv * rs;
         if constexpr (FAM == FAM_EXP_ANISO) {
 #pragma unroll
             for (int l = 0; l < D; ++l)
-                Dv[l] = g * sc[l] * E.inv_rho[l];
+                Dv[l] = g * sc[l];          // * 1/range_l
         } else {
-            Dv[0] = g * sp2 * E.inv_rho[0];
-            Dv[1] = g * sc[D - 1] * E.inv_rho[D - 1];
+            Dv[0] = g * sp2;                // * 1/range_space
+            Dv[1] = g * sc[D - 1];          // * 1/range_time
         }
     }
 }
 
+// the constant factor of range-derivative matrix r that pair_terms_r leaves out
+template <int FAM, int D>
+__device__ __forceinline__ double deriv_scale(const EvalParams &E, int r)
+{
+    if constexpr (FAM == FAM_MATERN)
+        return 1.0;
+    else if constexpr (FAM == FAM_MATERN25)
+        return E.inv_rho[0] * (1.0 / 3.0);
+    else if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15)
+        return E.inv_rho[0];
+    else if constexpr (FAM == FAM_EXP_ANISO)
+        return E.inv_rho[r];
+    else
+        return r == 0 ? E.inv_rho[0] : E.inv_rho[D - 1];
+}
+
+// compile-time loop: f(std::integral_constant<int, K>) for K0 <= K < K1 (register indices must be static)
+template <int K0, int K1, class F>
+__device__ __forceinline__ void static_for(F &&f)
+{
+    if constexpr (K0 < K1) {
+        f(std::integral_constant<int, K0>{});
+        static_for<K0 + 1, K1>(f);
+    }
+}
+
+// Static schedule of the row-owner pair phase: flat step k -> slot pair h (h == NH: the unpaired last
+// slot of an odd S) and step t within it.
 template <int G, int S>
-struct TileGeom {
-    static constexpr int CAP = G * S;
-    static constexpr int OPW = 32 / G;                 // observations per warp
-    static constexpr int TRI = CAP * (CAP + 1) / 2;    // packed lower triangle incl. diagonal
-    // column store: element (c, j), c >= j, of the (unscaled) factor lives at colbase(j) + c, columns
-    // packed back to back.  colbase(j) = -j(j+1)/2 (mod 16) when CAP = 32, so the 16 lanes of a group
-    // reading "their" columns at a common row hit 16 different 8-byte banks.
-    __host__ __device__ static constexpr int colbase(int j) { return j * (CAP - 1) - j * (j - 1) / 2; }
-    static constexpr int KL = TRI + 2; // one element past the last column may be read by a pair load
-    __host__ __device__ static constexpr int slot_of(int r) { return r / G; }
-    __host__ __device__ static constexpr int lane_of(int r) { return ((r / G) & 1) ? (G - 1 - r % G) : (r % G); }
+struct PairSched {
+    enum : int { ALL1 = 0, ALL0 = 1, MIXED = 2, ODD_MIXED = 3 };
+    static constexpr int NH = S / 2;
+    __host__ __device__ static constexpr int T(int h) { return (4 * h + 2) * G - 1; }
+    // h = 0: lane 0 owns the padding row 0 in slot 0, so its row a1 = 2G-1 needs one more step
+    __host__ __device__ static constexpr int steps(int h) { return h < NH ? T(h) - 2 + (h == 0 ? 1 : 0) : S * G - 2; }
+    __host__ __device__ static constexpr int total()
+    {
+        int n = 0;
+        for (int h = 0; h < NH + (S % 2); ++h)
+            n += steps(h);
+        return n;
+    }
+    static constexpr int NIT = total();
+    __host__ __device__ static constexpr int h_of(int k)
+    {
+        int h = 0;
+        while (k >= steps(h)) {
+            k -= steps(h);
+            ++h;
+        }
+        return h;
+    }
+    __host__ __device__ static constexpr int t_of(int k)
+    {
+        int h = 0;
+        while (k >= steps(h)) {
+            k -= steps(h);
+            ++h;
+        }
+        return k + 1;
+    }
+    __host__ __device__ static constexpr int kind(int k)
+    {
+        const int h = h_of(k), t = t_of(k);
+        if (h == NH)
+            return t < (S - 1) * G ? ALL1 : ODD_MIXED;
+        return t < (2 * h + 1) * G ? ALL1 : (t > (2 * h + 2) * G - 2 ? ALL0 : MIXED);
+    }
 };
 
 template <int G, int S, int D, int QD>
-struct TileSmem {
+struct LikSmem {
     using Geo = TileGeom<G, S>;
     static constexpr int DP = (D + 1) & ~1;                 // padded coordinate stride (16-byte rows)
     static constexpr int PTS = Geo::CAP * DP;               // scaled coordinates of the local frame
-    // K staging, the column store of the factorization and every D_j share ONE packing: element
-    // (a, c), a >= c, at colbase(c) + a (columns back to back).  The pair table walks the columns
-    // from the last one down, rows ascending, so the staging stores of a lane group are contiguous;
-    // the row loads (static c, lane-varying a) are contiguous as well.
+    // The column store of the factorization and every D_r share ONE packing: element (a, c), a >= c,
+    // at colbase(c) + a (columns back to back).
     static constexpr int DSZ = (Geo::TRI + 1) & ~1;
-    static constexpr int PER_OBS = PTS + Geo::KL + QD * DSZ;
-    static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
-    // Local row 0 is ALWAYS a padding row (tiers serve m+1 <= CAP-1), so nothing is computed for it.
-    // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
-    // multiple of NI*G with copies of the last pair; entry = a << 24 | c << 16 | (colbase(c) + a)
-    static constexpr int TOFF = (Geo::CAP - 1) * (Geo::CAP - 2) / 2; // pairs among local rows 1..CAP-1
-    static constexpr int NI = TILED_NI;                     // pairs in flight per lane in the pair loop
-    static constexpr int TPAD = (TOFF + NI * G - 1) / (NI * G) * (NI * G);
+    static constexpr int RAW = PTS + Geo::KL + QD * DSZ;
+    // Per-observation stride = 16/OPW (mod 16) doubles: the 16-byte broadcast chunks of the OPW lane
+    // groups fall on different banks AND the G-contiguous stores of the groups tile the 16 8-byte
+    // banks exactly twice (measured conflict-free: tools/micro/lds_groups.cu).
+    static constexpr int WANT = (Geo::OPW >= 2) ? 16 / Geo::OPW : 0;
+    static constexpr int PER_OBS = RAW + ((WANT - RAW % 16) + 16) % 16;
+    static constexpr int TOTAL = VB_EXPTAB + TILED_WPB * Geo::OPW * PER_OBS;
 };
 
-// blocks per SM (one warp per block) the register budget of a tier is tuned for: the rows a lane
-// keeps in registers take G*S(S+1) 32-bit registers; 168 registers = 3 warps per SM sub-partition
-__host__ __device__ constexpr int tiled_min_blocks(int G, int S)
+// phase boundary: with several warps per block they walk the (straight-line, > 64 KB) instruction stream
+// together, so one instruction-cache fill serves all of them
+__device__ __forceinline__ void phase_sync()
 {
-    return (G * S * (S + 1) <= 48) ? 16 : ((G * S * (S + 1) <= 96) ? 12 : 8);
+    if (TILED_WPB > 1)
+        __syncthreads();
+    else
+        __syncwarp();
 }
 
 template <int G, int S, int FAM, int D, int P>
-__global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kernel(const EvalParams E)
+__global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
 {
     using Geo = TileGeom<G, S>;
     using FT = FamTraits<FAM, D>;
     constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
-    using SM = TileSmem<G, S, D, QD>;
+    using SM = LikSmem<G, S, D, QD>;
     constexpr int DP = SM::DP, DSZ = SM::DSZ;
     constexpr int L = (1 + Q) * (2 + P + P * P) + Q * Q;
     constexpr int NACC = (L + G - 1) / G;
@@ -160,56 +218,73 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
     static_assert(CAP % 2 == 0 && CAP <= 128, "tier geometry");
 
     extern __shared__ double smem[];
-    double *etab = smem;                             // 2^(j/64), j < 64
-    const int lane = threadIdx.x;
+    double *etab = smem;                             // sigma^2 2^(j/32), j < 32
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
     const int g = lane / G, lg = lane % G;
-    double *obs = smem + VB_EXPTAB + g * SM::PER_OBS;
+    double *obs = smem + VB_EXPTAB + (warp * OPW + g) * SM::PER_OBS;
     double *pts = obs;                               // CAP x DP scaled coordinates of the local frame
-    double *KLs = obs + SM::PTS;                     // packed K staging, then the column store of L
-    double *Dms = KLs + Geo::KL;                     // QD packed strict-lower derivative matrices (+ zero slot)
+    double *KLs = obs + SM::PTS;                     // the column store of the factorization
+    double *Dms = KLs + Geo::KL;                     // QD packed range-derivative matrices
 
-    for (int t = lane; t < VB_EXPTAB; t += 32)
-        etab[t] = exp2((double)t * (1.0 / VB_EXPTAB));
-    // diagonal and column 0 of every D_j are zero and never written by the pair loop
+    for (int t = threadIdx.x; t < VB_EXPTAB; t += 32 * TILED_WPB)
+        etab[t] = E.sig2 * exp2((double)t * (1.0 / VB_EXPTAB));
+    // never written again: diagonal and column 0 of every D_r (zero), column 0 of the column store
+    for (int a = lg; a < CAP; a += G) {
 #pragma unroll
-    for (int j = 0; j < QD; ++j)
-        for (int a = lg; a < CAP; a += G) {
+        for (int j = 0; j < QD; ++j) {
             Dms[j * DSZ + a] = 0.0;
             Dms[j * DSZ + Geo::colbase(a) + a] = 0.0;
         }
+        KLs[a] = 0.0;
+    }
     int rowi[S], colb_r[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         rowi[s] = s * G + ((s & 1) ? (G - 1 - lg) : lg);
         colb_r[s] = Geo::colbase(rowi[s]);
     }
+    double dscale[QD];
+#pragma unroll
+    for (int r = 0; r < QD; ++r)
+        dscale[r] = deriv_scale<FAM, D>(E, r);
     double acc[NACC];
 #pragma unroll
     for (int t = 0; t < NACC; ++t)
         acc[t] = 0.0;
-    __syncwarp();
+    phase_sync();
 
+    // experiment (profiles/r1_experiments.md): an initial offset between the resident blocks of an SM, to rule out
+    // phase-locking of the warps (all in the FP64-heavy pair phase, then all in the factorization).  No effect.
+    if (TILED_STAGGER_NS > 0) {
+        const unsigned slot = blockIdx.x / E.sm_count; // k-th block of its SM (round-robin placement)
+        for (unsigned w = 0; w < slot; ++w)
+            __nanosleep(TILED_STAGGER_NS);
+    }
     const int64_t nbatch = (E.i1 - E.i0 + OPW - 1) / OPW;
-    for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * TILED_WPB;
+    // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
+    for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
+        const int64_t batch = batch0 + warp;
         const int64_t i = E.i0 + batch * OPW + g;
         const bool active = i < E.i1;
         const int64_t *nrow = E.nn + (active ? (i - E.nn_row0) : 0) * E.mp1;
 
         // ---- gather: local index a <-> neighbor column CAP-1-a (observation last).  Coordinates are
-        //      stored divided by the range of their axis.  Padding rows: diagonal 1, data 0. ----
-        double rhs[1 + P][S];
+        //      kept divided by the range of their axis.  Padding rows: diagonal 1, data 0, far away. ----
+        double rhs[1 + P][S], pa[S][D], Kr[S][CAP];
         int nlive = 0;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int a = rowi[s], col = CAP - 1 - a;
             int64_t idx = -1;
             if (active && col < E.mp1)
-                idx = nrow[col];
+                idx = (TILED_ABLATE & 16) ? (int64_t)((i * 7 + col * 13) % 1000) : nrow[col];
             const bool live = idx >= 0;
             double cx[DP];
 #pragma unroll
             for (int l = 0; l < DP; ++l)
                 cx[l] = 0.0;
+            cx[0] = 1e30 * (double)(a + 1);
             rhs[0][s] = 0.0;
 #pragma unroll
             for (int b = 0; b < P; ++b)
@@ -225,125 +300,156 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
                     rhs[1 + b][s] = r[D + 1 + b];
             }
 #pragma unroll
+            for (int l = 0; l < D; ++l)
+                pa[s][l] = cx[l];
+#pragma unroll
             for (int l = 0; l < DP; l += 2)
                 *reinterpret_cast<double2 *>(pts + a * DP + l) = make_double2(cx[l], cx[l + 1]);
-            KLs[colb_r[s] + a] = live ? E.diag : 1.0;
+            // diagonal block of the slot: the diagonal entry, zeros above it (never used, must be finite)
+            const double dg = live ? E.diag : 1.0;
+#pragma unroll
+            for (int c = s * G; c < (s + 1) * G; ++c)
+                Kr[s][c] = (c == a) ? dg : 0.0;
+            if (s > 0)
+                Kr[s][0] = 0.0; // column 0 belongs to the padding row 0
             const unsigned bal = __ballot_sync(FULLMASK, live);
             nlive += __popc((G == 32) ? bal : ((bal >> (g * G)) & ((1u << (G & 31)) - 1u)));
         }
         const int pad = CAP - nlive; // identity rows at the front of the local frame
-        __syncwarp();
+        phase_sync();
 
-        // ---- pair terms.  The table lists the off-diagonal pairs (a > c) by DESCENDING c, so the
-        //      k(k-1)/2 pairs of the live points come first; they are dealt round-robin to the lanes
-        //      of the group, two independent pairs per iteration (ILP), and staged in the packed
-        //      triangles.  Pairs that touch a padding row are just zero-filled. ----
-        const int nlp = nlive * (nlive - 1) / 2;
+        // ---- pair terms, row-owner.  Slot pair (s0, s1) = (2h, 2h+1): rows a0 = 2hG + lg and
+        //      a1 = (2h+2)G - 1 - lg, a0 + a1 = T for every lane.  Step t: pair (a1, t) while t < a1,
+        //      afterwards pair (a0, T-1-t).  Column 0 (t = 0, t = T-1) is the padding row: skipped.
+        //      The steps are processed NI at a time -- all loads, then NI independent evaluation
+        //      chains (the compiler interleaves them; one chain alone is ~25 dependent FP64
+        //      instructions), then all stores -- because a store to D_r between two loads of the
+        //      point table would serialise the chains (the compiler cannot prove they do not alias). ----
         {
-            constexpr int NI = SM::NI; // independent pairs in flight per lane (ILP; registers are free here)
-            unsigned nxt[NI];
+            using PS = PairSched<G, S>;
+            constexpr int NI = TILED_RNI;
+            if (!(TILED_ABLATE & 1))
+            static_for<0, (PS::NIT + NI - 1) / NI>([&](auto chunk_c) {
+                constexpr int k0 = decltype(chunk_c)::value * NI;
+                double dl[NI][D];
+                bool prv[NI];
+                static_for<0, NI>([&](auto u_c) {
+                    constexpr int u = decltype(u_c)::value, k = k0 + u;
+                    if constexpr (k < PS::NIT) {
+                        constexpr int h = PS::h_of(k), t = PS::t_of(k), kind = PS::kind(k);
+                        constexpr int s1 = (h < PS::NH) ? 2 * h + 1 : S - 1, s0 = (h < PS::NH) ? 2 * h : S - 1;
+                        constexpr int c1 = t, c0 = (h < PS::NH) ? PS::T(h) - 1 - t : t;
+                        bool pr = true;
+                        if constexpr (kind == PS::MIXED)
+                            pr = lg < (2 * h + 2) * G - 1 - t; // t < a1
+                        if constexpr (kind == PS::ODD_MIXED)
+                            pr = t < rowi[S - 1];
+                        prv[u] = pr;
+                        const double *pc = pts + ((kind == PS::ALL0) ? c0 : (kind == PS::MIXED ? (pr ? c1 : c0) : c1)) * DP;
+                        auto own = [&](int l) { // coordinate l of the row point of this step
+                            return (kind == PS::ALL0) ? pa[s0][l] : (kind == PS::MIXED ? (pr ? pa[s1][l] : pa[s0][l]) : pa[s1][l]);
+                        };
 #pragma unroll
-            for (int h = 0; h < NI; ++h)
-                nxt[h] = E.pair_tab[lg + h * G];
-            for (int t0 = lg; t0 < nlp; t0 += NI * G) {
-                unsigned ent[NI];
-#pragma unroll
-                for (int h = 0; h < NI; ++h)
-                    ent[h] = nxt[h];
-                if (t0 + NI * G < SM::TPAD) { // prefetch the next entries (L1-resident table)
-#pragma unroll
-                    for (int h = 0; h < NI; ++h)
-                        nxt[h] = E.pair_tab[t0 + (NI + h) * G];
-                }
-                double Kv[NI], Dv[NI][QD];
-#pragma unroll
-                for (int h = 0; h < NI; ++h) {
-                    const double *pa = pts + (ent[h] >> 24) * DP;
-                    const double *pc = pts + ((ent[h] >> 16) & 255) * DP;
-                    double dl[D];
-#pragma unroll
-                    for (int l = 0; l < DP; l += 2) {
-                        const double2 va = *reinterpret_cast<const double2 *>(pa + l);
-                        const double2 vc = *reinterpret_cast<const double2 *>(pc + l);
-                        dl[l] = va.x - vc.x;
-                        if (l + 1 < D)
-                            dl[l + 1 < D ? l + 1 : l] = va.y - vc.y;
+                        for (int l = 0; l < DP; l += 2) {
+                            const double2 vc = *reinterpret_cast<const double2 *>(pc + l);
+                            dl[u][l] = own(l) - vc.x;
+                            if (l + 1 < D)
+                                dl[u][l + 1 < D ? l + 1 : l] = own(l + 1 < D ? l + 1 : l) - vc.y;
+                        }
                     }
-                    pair_terms_s<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
-                }
-                // entries past nlp in the last iteration belong to padding pairs: they are written
-                // here and overwritten with zeros below (after the warp sync)
+                });
+                double Kv[NI], Dv[NI][QD];
+                static_for<0, NI>([&](auto u_c) {
+                    constexpr int u = decltype(u_c)::value;
+                    if constexpr (k0 + u < PS::NIT)
+                        pair_terms_r<FAM, D>(E, etab, dl[u], Kv[u], Dv[u]);
+                });
+                static_for<0, NI>([&](auto u_c) {
+                    constexpr int u = decltype(u_c)::value, k = k0 + u;
+                    if constexpr (k < PS::NIT) {
+                        constexpr int h = PS::h_of(k), t = PS::t_of(k), kind = PS::kind(k);
+                        constexpr int s1 = (h < PS::NH) ? 2 * h + 1 : S - 1, s0 = (h < PS::NH) ? 2 * h : S - 1;
+                        constexpr int c1 = t, c0 = (h < PS::NH) ? PS::T(h) - 1 - t : t;
+                        const bool pr = prv[u];
+                        if constexpr (kind == PS::ALL1) {
+                            Kr[s1][c1] = Kv[u];
 #pragma unroll
-                for (int h = 0; h < NI; ++h) {
-                    const int kidx = ent[h] & 0xffff;
-                    KLs[kidx] = Kv[h];
+                            for (int r = 0; r < QD; ++r)
+                                Dms[r * DSZ + Geo::colbase(c1) + rowi[s1]] = Dv[u][r];
+                        } else if constexpr (kind == PS::ALL0) {
+                            Kr[s0][c0] = Kv[u];
 #pragma unroll
-                    for (int j = 0; j < QD; ++j)
-                        Dms[j * DSZ + kidx] = Dv[h][j];
-                }
-            }
-            __syncwarp();
-            for (int t = nlp + lg; t < SM::TOFF; t += G) {
-                const unsigned e0 = E.pair_tab[t];
-                const int kidx = e0 & 0xffff;
-                KLs[kidx] = 0.0;
+                            for (int r = 0; r < QD; ++r)
+                                Dms[r * DSZ + Geo::colbase(c0) + rowi[s0]] = Dv[u][r];
+                        } else if constexpr (kind == PS::MIXED) {
+                            Kr[s1][c1] = pr ? Kv[u] : Kr[s1][c1];
+                            if constexpr (c0 > 0) {
+                                Kr[s0][c0] = pr ? Kr[s0][c0] : Kv[u];
+                                const int dst = pr ? (Geo::colbase(c1) + rowi[s1]) : (Geo::colbase(c0) + rowi[s0]);
 #pragma unroll
-                for (int j = 0; j < QD; ++j)
-                    Dms[j * DSZ + kidx] = 0.0;
-            }
+                                for (int r = 0; r < QD; ++r)
+                                    Dms[r * DSZ + dst] = Dv[u][r];
+                            } else if (pr) { // column 0 is the padding row: only the (a1, t) pairs are real
+#pragma unroll
+                                for (int r = 0; r < QD; ++r)
+                                    Dms[r * DSZ + Geo::colbase(c1) + rowi[s1]] = Dv[u][r];
+                            }
+                        } else { // unpaired last slot, steps where some lanes have run out of pairs
+                            Kr[s1][c1] = pr ? Kv[u] : Kr[s1][c1];
+                            if (pr) {
+#pragma unroll
+                                for (int r = 0; r < QD; ++r)
+                                    Dms[r * DSZ + Geo::colbase(c1) + rowi[s1]] = Dv[u][r];
+                            }
+                        }
+                    }
+                });
+            });
         }
-        __syncwarp();
-
-        // ---- own rows into registers ----
-        double Kr[S][CAP];
-#pragma unroll
-        for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int c = 0; c < (s + 1) * G; ++c)
-                Kr[s][c] = KLs[Geo::colbase(c) + rowi[s]];
-        __syncwarp();
+        phase_sync();
 
         // ---- square-root-free factorization K = Lt D Lt^T (Lt unit lower, D = diag(d)), right-looking,
         //      with the forward substitutions of y and X fused in.  The Cholesky factor of the reference
         //      is B = Lt D^(1/2); working with Lt and d keeps sqrt AND the diagonal scalings out of every
-        //      dependent chain: at step j the UNSCALED column j (d_j on top) goes to the column store
-        //      as soon as the previous update is done, and 1/d_j is formed by all lanes from the
-        //      broadcast read, in parallel with the rest of the column loads. ----
+        //      dependent chain.  The chain of a step is   update of column j+1 -> store column j+1 ->
+        //      broadcast read of its head (d_{j+1}, Kt(j+2, j+1)) -> 1/d_{j+1} -> multipliers;
+        //      with LOOK-AHEAD: step j first updates column j+1 only, publishes it and starts the
+        //      reciprocal of the next pivot, and only then applies column j to the rest of the trailing
+        //      matrix, so the bulk of the rank-1 update fills the latency of the chain. ----
         double invd[S]; // 1/d_a of the own rows
 #pragma unroll
         for (int s = 0; s < S; ++s)
             invd[s] = 1.0;
         int failpiv = 0;
-#pragma unroll
-        for (int j = 1; j < CAP - 1; ++j) { // local row 0 is always padding: step 0 is the identity
-            const int sj = j / G;
-            const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
-            const double *col = KLs + Geo::colbase(j);
+        // head of column j: pivot d_j and the next one or two entries.  Pairs (c0, c0+1) of a column are
+        // read as one 128-bit broadcast load; cs(j) = first index of column j that starts an aligned pair.
+        double Lo[S], xr[1 + P], hd, h1, h2 = 0.0;
+        auto publish = [&](const int j) { // store column j, fetch (Lt^-1 rhs)_j (final once step j-1 is applied)
+            const int sj = j / G, oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
 #pragma unroll
             for (int s = 0; s < S; ++s)
                 if ((s + 1) * G - 1 >= j && rowi[s] >= j)
                     KLs[Geo::colbase(j) + rowi[s]] = Kr[s][j];
-            double xr[1 + P];
 #pragma unroll
             for (int r = 0; r < 1 + P; ++r)
-                xr[r] = __shfl_sync(FULLMASK, rhs[r][sj], oj, G); // (Lt^-1 rhs)_j is final at step j
+                xr[r] = __shfl_sync(FULLMASK, rhs[r][sj], oj, G);
             __syncwarp();
-            // pairs (c0, c0+1) are read as one 128-bit broadcast load; the parity of the first pair is
-            // static (colbase(j) + c0 must be even)
+            const double *col = KLs + Geo::colbase(j);
             const int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
-            double dj;
-            if (cs != j)
-                dj = col[j];
-            double2 v0;
             if (cs == j) {
-                v0 = *reinterpret_cast<const double2 *>(col + j);
-                dj = v0.x;
+                const double2 v = *reinterpret_cast<const double2 *>(col + j);
+                hd = v.x;
+                h1 = v.y;
+            } else {
+                hd = col[j];
+                const double2 v = *reinterpret_cast<const double2 *>(col + j + 1);
+                h1 = v.x;
+                h2 = v.y;
             }
-            failpiv = (failpiv == 0 && dj <= E.piv_floor) ? (j + 1) : failpiv;
-            const double rj = rcp_pos(dj);
-            // Lo[s] = Lt[row][j] for rows below the pivot row, exactly 0 for finished rows, so the
-            // updates need no per-row predicates (a finished row just adds -0 * x)
-            double Lo[S];
+            failpiv = (failpiv == 0 && hd <= E.piv_floor) ? (j + 1) : failpiv;
+        };
+        auto multipliers = [&](const int j) { // Lo[s] = Lt[row][j] below the pivot row, exactly 0 for finished rows
+            const double rj = rcp_pos3(hd);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if ((s + 1) * G - 1 > j) {
@@ -356,30 +462,70 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
                 if ((s + 1) * G - 1 >= j)
                     invd[s] = (rowi[s] == j) ? rj : invd[s];
             }
+        };
+        if (!(TILED_ABLATE & 2)) {
+        publish(1); // local row 0 is always padding: step 0 is the identity
+        multipliers(1);
+        }
+        if (!(TILED_ABLATE & 2))
+        static_for<1, CAP - 1>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            constexpr int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
+            const double *col = KLs + Geo::colbase(j);
+            // column j is applied with the multipliers of THIS step; the look-ahead below overwrites
+            // Lo / xr / h1 / h2 with those of step j+1, so keep copies (SSA renames, no moves)
+            double Lc[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                Lc[s] = Lo[s];
+            const double g2 = h2;
+            // the pair loads of the rest of column j run PD loads ahead of the FMAs that consume them
+            // (left to itself the compiler issues each load right before its first use and the warp eats
+            // the full shared-memory latency once per load: measured, profiles/)
+            constexpr int cb0 = (cs == j) ? j + 2 : j + 3;
+            constexpr int NPAIR = (CAP - cb0 + 1) / 2;
+            constexpr int PD = TILED_PD;
+            double2 ring[PD];
+#pragma unroll
+            for (int i = 0; i < PD; ++i)
+                if (i < NPAIR)
+                    ring[i] = *reinterpret_cast<const double2 *>(col + cb0 + 2 * i);
 #pragma unroll
             for (int r = 0; r < 1 + P; ++r)
 #pragma unroll
                 for (int s = 0; s < S; ++s)
                     if ((s + 1) * G - 1 > j)
-                        rhs[r][s] = fma(-Lo[s], xr[r], rhs[r][s]);
-            if (cs == j) {
+                        rhs[r][s] = fma(-Lc[s], xr[r], rhs[r][s]);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if ((s + 1) * G - 1 >= j + 1)
+                    Kr[s][j + 1] = fma(-Lc[s], h1, Kr[s][j + 1]);
+            if constexpr (j + 1 < CAP - 1)
+                publish(j + 1);
+            // the rest of the trailing update with column j
+            if constexpr (cs != j && j + 2 < CAP) {
 #pragma unroll
                 for (int s = 0; s < S; ++s)
-                    if ((s + 1) * G - 1 >= j + 1)
-                        Kr[s][j + 1] = fma(-Lo[s], v0.y, Kr[s][j + 1]);
+                    if ((s + 1) * G - 1 >= j + 2)
+                        Kr[s][j + 2] = fma(-Lc[s], g2, Kr[s][j + 2]);
             }
 #pragma unroll
-            for (int c0 = (cs == j) ? j + 2 : j + 1; c0 < CAP; c0 += 2) {
-                const double2 v = *reinterpret_cast<const double2 *>(col + c0);
+            for (int i = 0; i < NPAIR; ++i) {
+                const int c0 = cb0 + 2 * i;
+                const double2 v = ring[i % PD];
+                if (i + PD < NPAIR)
+                    ring[i % PD] = *reinterpret_cast<const double2 *>(col + c0 + 2 * PD);
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     if ((s + 1) * G - 1 >= c0)
-                        Kr[s][c0] = fma(-Lo[s], v.x, Kr[s][c0]);
+                        Kr[s][c0] = fma(-Lc[s], v.x, Kr[s][c0]);
                     if (c0 + 1 < CAP && (s + 1) * G - 1 >= c0 + 1)
-                        Kr[s][c0 + 1] = fma(-Lo[s], v.y, Kr[s][c0 + 1]);
+                        Kr[s][c0 + 1] = fma(-Lc[s], v.y, Kr[s][c0 + 1]);
                 }
             }
-        }
+            if constexpr (j + 1 < CAP - 1)
+                multipliers(j + 1);
+        });
         // last pivot d_e (row CAP-1 = the observation itself): nothing left to update
         constexpr int se = S - 1;
         constexpr int oe = Geo::lane_of(CAP - 1);
@@ -394,6 +540,7 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
         //      matrices, tt_r += D_r[., l] ut_l, so D_r u needs no separate mat-vec pass.  Element
         //      (a, l) of the symmetric D_r lives at colbase(a) + l (a < l) or colbase(l) + a (a >= l;
         //      the diagonal holds zeros). ----
+        phase_sync();
         double sb[S], eb[S], rr[QD + 1][S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -403,31 +550,61 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
             for (int r = 0; r < QD; ++r)
                 rr[r][s] = 0.0;
         }
-#pragma unroll
-        for (int l = CAP - 1; l >= 1; --l) {
-            const int sl = l / G;
-            const int ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
-            const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
+        // the loads of step l-1 are issued before the shuffle of step l is waited for (they do not depend
+        // on ut), so the dependent chain of a step is one FMA + one shuffle
+        double Kc[S], Dc[QD][S];
+        auto fetch = [&](const int l, double (&Kl)[S], double (&Dl)[QD][S]) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const bool above = rowi[s] < l;
-                if (s * G < l) { // slot has rows < l
-                    const double Klj = above ? KLs[colb_r[s] + l] : 0.0;
-                    sb[s] = fma(Klj, ul, sb[s]);
-                }
+                Kl[s] = 0.0;
+                if (s * G < l) // slot has rows < l
+                    Kl[s] = above ? KLs[colb_r[s] + l] : 0.0;
                 const int addr = above ? (colb_r[s] + l) : (Geo::colbase(l) + rowi[s]);
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
-                    rr[r][s] = fma(Dms[r * DSZ + addr], ul, rr[r][s]);
+                    Dl[r][s] = Dms[r * DSZ + addr];
             }
-        }
+        };
+        fetch(CAP - 1, Kc, Dc);
+        if (!(TILED_ABLATE & 4))
+        static_for<0, CAP - 1>([&](auto ic) {
+            constexpr int l = CAP - 1 - decltype(ic)::value;
+            constexpr int sl = l / G, ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
+            double Kn[S], Dn[QD][S];
+            if constexpr (l > 1)
+                fetch(l - 1, Kn, Dn);
+            const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
 #pragma unroll
-        for (int s = 0; s < S; ++s) // padding rows: ut = 0 whatever was read
+            for (int s = 0; s < S; ++s) {
+                if (s * G < l)
+                    sb[s] = fma(Kc[s], ul, sb[s]);
+#pragma unroll
+                for (int r = 0; r < QD; ++r)
+                    rr[r][s] = fma(Dc[r][s], ul, rr[r][s]);
+            }
+            if constexpr (l > 1) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    Kc[s] = Kn[s];
+#pragma unroll
+                    for (int r = 0; r < QD; ++r)
+                        Dc[r][s] = Dn[r][s];
+                }
+            }
+        });
+#pragma unroll
+        for (int s = 0; s < S; ++s) { // padding rows: ut = 0 whatever was read
             rr[QD][s] = (rowi[s] < pad) ? 0.0 : fma(-sb[s], invd[s], eb[s]);
+#pragma unroll
+            for (int r = 0; r < QD; ++r)
+                rr[r][s] *= dscale[r];
+        }
 
+        phase_sync();
         // ---- [tt_1..tt_QD, ut] through Lt^-1 (unit-diagonal forward sweeps on the register-resident rows) ----
 #pragma unroll
-        for (int j = 1; j < CAP - 1; ++j) {
+        for (int j = 1; j < ((TILED_ABLATE & 8) ? 1 : CAP - 1); ++j) {
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
             double Lm[S];
@@ -460,6 +637,7 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
                 s0 = fma(x[s], y[s], s0);
             return gsum(s0);
         };
+        phase_sync();
         const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
         const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
         const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G) * rho_e;
@@ -529,7 +707,7 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
             if (E.fail_rows)
                 E.fail_rows[i - E.i0] = failpiv - pad;
         }
-        __syncwarp();
+        phase_sync();
     }
 
     // ---- block partial: add the groups of this warp in fixed order, one row of `partials` per block ----
@@ -541,15 +719,18 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_kern
             v += __shfl_xor_sync(FULLMASK, v, off);
         const int o = t * G + lg;
         if (g == 0 && o < L)
-            E.partials[(size_t)blockIdx.x * L + o] = v;
+            E.partials[((size_t)blockIdx.x * TILED_WPB + warp) * L + o] = v;
     }
 }
+
+#include "kernel_tiled_pt.cuh"
 
 // ---------------------------------------------------------------------------
 // host side: instance table and launch
 // ---------------------------------------------------------------------------
 struct TiledInstance {
-    int g, s, cap, family, d, p;
+    int g, s, cap, family, d, p, wpb;
+    int pair_table; // 1: the pair-table variant (kernel_tiled_pt.cuh) -- needs EvalParams::pair_tab
     void (*kernel)(const EvalParams);
     int smem_doubles;
     const char *name;
@@ -557,7 +738,14 @@ struct TiledInstance {
 
 #define TILED_INST(G_, S_, FAM_, D_, P_)                                                                        \
     {                                                                                                           \
-        G_, S_, (G_) * (S_), FAM_, D_, P_, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
-            TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, TILED_WPB, 0, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
+            LikSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                 \
             "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                            \
+    }
+
+#define TILED_INST_PT(G_, S_, FAM_, D_, P_)                                                                     \
+    {                                                                                                           \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, 1, vecchia_tiled_pt_kernel<G_, S_, FAM_, D_, P_>,                         \
+            TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
+            "vecchia_tiled_pt_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                         \
     }
