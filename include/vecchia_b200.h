@@ -162,6 +162,24 @@ int vb200_krige(vb200_problem *prob, int family, const double *theta, int q, con
                 const double *locs_star, const int64_t *nn_star, int64_t npred, int m_pred, int latent,
                 double *mean_resid, double *var, int64_t *first_fail);
 
+/* ---- conditional simulation ------------------------------ */
+/*
+ * Draw y from the neighbour-conditioned model itself; replaces the sequential loop of the reference's
+ * oracle.simulate_nn_gp (oracle.py:102-140): y_i = x_i' beta + E[r_i | y of its neighbours] +
+ * sqrt(max(var_i, 0)) xi_i with var_i = variance*(1+nugget) - k' K^-1 k.  `prob` must hold the neighbour
+ * rows of ALL n observations; xi (n) are the standard normal draws (the reference uses
+ * numpy.random.Generator(PCG64(seed)).standard_normal(n): generate them on the host for identical
+ * output).  Observation i only depends on observations of lower dependency LEVEL (level = 1 + max level of
+ * its neighbours), so the device runs one launch per level: order (n) lists the observations by (level,
+ * index), level_ptr (nlevels + 1) delimits the levels (vbh_dependency_levels of the host library builds
+ * both).  y_out (n, host or device) receives the draw, and the response held by `prob` is REPLACED by it,
+ * so the likelihood of the simulated field can be evaluated on the same handle.  Host or device pointers
+ * for xi / order; level_ptr is read on the host.  *first_fail as in vb200_krige.
+ */
+int vb200_simulate(vb200_problem *prob, int family, const double *theta, int q, const double *beta,
+                   const double *xi, const int64_t *order, const int64_t *level_ptr, int64_t nlevels,
+                   double *y_out, int64_t *first_fail);
+
 /* number of kernel launches the last vb200_eval* call enqueued, and the name of the
  * main kernel variant (for bench.py's gpu_launches / roofline bookkeeping) */
 int vb200_last_launch_count(const vb200_problem *prob);

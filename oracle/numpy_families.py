@@ -159,3 +159,33 @@ def dense_loglik(family, theta, y, X, locs):
     r = hy - hX @ beta
     n = len(y)
     return -0.5 * (n * np.log(2 * np.pi) + 2.0 * np.log(np.diag(L)).sum() + r @ r), beta
+
+
+def simulate_nn_gp(family, theta, beta, locs, X, nn, seed):
+    """Sequential conditional draw from the neighbour-conditioned model -- restates the reference's
+    oracle.simulate_nn_gp (/root/reference/pkg/src/vecchiagp/oracle.py:102-140) for every family of this
+    package (locs are WORKING coordinates; the local matrix comes from cov_and_derivs, nugget on the diagonal).
+    Pure-Python loop: small cases only."""
+    theta = np.asarray(theta, dtype=np.float64)
+    locs = np.atleast_2d(np.asarray(locs, dtype=np.float64))
+    X = np.atleast_2d(np.asarray(X, dtype=np.float64))
+    n = locs.shape[0]
+    xi = np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
+    mean = X @ np.atleast_1d(beta)
+    y = np.empty(n)
+    var_prior = theta[0] * (1.0 + theta[-1])
+    for i in range(n):
+        row = nn[i]
+        row = row[row >= 0]
+        nbrs = row[1:][::-1]
+        k = nbrs.shape[0]
+        if k == 0:
+            y[i] = mean[i] + np.sqrt(var_prior) * xi[i]
+            continue
+        K, _ = cov_and_derivs(family, theta, np.vstack([locs[nbrs], locs[i]]))
+        L = cholesky(K[:k, :k], lower=True)
+        w = solve_triangular(L, K[:k, k], lower=True)
+        cond_mean = mean[i] + w @ solve_triangular(L, y[nbrs] - mean[nbrs], lower=True)
+        y[i] = cond_mean + np.sqrt(max(var_prior - w @ w, 0.0)) * xi[i]
+    return y
+

@@ -6,8 +6,9 @@ from .errors import (DegenerateInformation, DeviceUnavailable, DimensionMismatch
 from .model import CovarianceParameters, Dataset, FitResult, ModelSpec, normalize_backend, validate_dataset
 from .covariance import FAMILY_NAMES, covariance_registry, validate_parameters
 from .preprocess import (NeighborArray, Ordering, embed_lonlat, find_ordered_neighbors, identity_ordering,
-                         lonlat_to_xyz, maxmin_ordering, random_permutation, reorder_dataset)
-from . import engine, inference, io, predict
+                         lonlat_to_xyz, maxmin_ordering, random_permutation, reorder_dataset, dependency_levels)
+from . import engine, inference, io, predict, simulate
+from .simulate import simulate_nn_gp
 from .predict import PredictionSet, krige, rmse
 from .engine import VecchiaParts, active_core_name, available_cores
 from .inference import ProfiledEvaluation, assemble, default_start, evaluate, fisher_step, fit, to_log_scale

@@ -39,6 +39,8 @@ _SIGNATURES = {
     "vb200_eval_rows": (c_int, [c_void_p, c_int, _dp, c_int, c_double, c_int64, c_int64, _dp, POINTER(c_int32)]),
     "vb200_krige": (c_int, [c_void_p, c_int, _dp, c_int, _dp, c_void_p, c_void_p, c_int64, c_int, c_int, _dp, _dp,
                             POINTER(c_int64)]),
+    "vb200_simulate": (c_int, [c_void_p, c_int, _dp, c_int, _dp, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                               POINTER(c_int64)]),
     "vb200_last_launch_count": (c_int, [c_void_p]),
     "vb200_last_kernel_name": (c_char_p, [c_void_p]),
     "vb200_tiled_instance_count": (c_int, []),

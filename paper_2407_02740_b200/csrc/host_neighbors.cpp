@@ -533,4 +533,40 @@ int vbh_neighbors_grid(const double *locs, int64_t n, int d, int m, int workers,
     return vbh_neighbors_grid_rows(locs, n, d, m, workers, 0, n, out);
 }
 
+// Dependency levels of the ordered-neighbor DAG (row i conditions on earlier rows only): level(i) =
+// 1 + max level of its neighbors, 0 for a row without neighbors.  Observations of one level are mutually
+// independent given the lower levels -- the schedule of the device conditional simulator.
+// order (n): observation indices sorted by (level, index); level_ptr (n + 1 entries allocated by the
+// caller, nlevels + 1 used): order[level_ptr[l] .. level_ptr[l+1]) is level l.  Returns nlevels, -1 on a
+// malformed table (a neighbor index >= its row).
+int64_t vbh_dependency_levels(const int64_t *nn, int64_t n, int mp1, int64_t *order, int64_t *level_ptr)
+{
+    std::vector<int32_t> level((size_t)n);
+    int64_t nlev = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t lv = 0;
+        const int64_t *row = nn + i * mp1;
+        for (int c = 1; c < mp1; ++c) {
+            const int64_t j = row[c];
+            if (j < 0)
+                break;
+            if (j >= i)
+                return -1;
+            lv = std::max(lv, level[(size_t)j] + 1);
+        }
+        level[(size_t)i] = lv;
+        nlev = std::max<int64_t>(nlev, lv + 1);
+    }
+    for (int64_t l = 0; l <= nlev; ++l)
+        level_ptr[l] = 0;
+    for (int64_t i = 0; i < n; ++i)
+        ++level_ptr[level[(size_t)i] + 1];
+    for (int64_t l = 0; l < nlev; ++l)
+        level_ptr[l + 1] += level_ptr[l];
+    std::vector<int64_t> cursor(level_ptr, level_ptr + nlev);
+    for (int64_t i = 0; i < n; ++i)
+        order[cursor[(size_t)level[(size_t)i]]++] = i;
+    return nlev;
+}
+
 } // extern "C"

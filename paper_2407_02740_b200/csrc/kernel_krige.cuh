@@ -22,6 +22,14 @@ struct KrigeParams {
     double beta[VB_MAXP];     // mean parameters: residual = y - X beta is formed in the gather
     double *mean_resid;       // out (npred): conditional mean of the residual at the point
     double *var;              // out (npred): conditional variance (not clamped)
+    // conditional SIMULATION (the reference's simulate_nn_gp; file:line in include/vecchia_b200.h): when sim_order is set,
+    // point t is training observation i = sim_order[t]; its neighbours are columns 1.. of row i of the
+    // training table, its location the one of record i, and instead of (mean_resid, var) the kernel writes
+    // y_i = x_i' beta + E[r_i | neighbours] + sqrt(max(var_i, 0)) xi_i into record i and into sim_y[i].
+    const int64_t *sim_order;
+    const double *xi;
+    double *sim_y;
+    double *rec_w;            // the (writable) point records of the problem
 };
 
 template <int G, int S, int D>
@@ -65,7 +73,9 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_krige_kern
     for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
         const int64_t t = batch * OPW + g;
         const bool active = t < Q.npred;
-        const int64_t *nrow = Q.nn_star + (active ? t : 0) * Q.m_pred;
+        const bool sim = Q.sim_order != nullptr;
+        const int64_t isim = (sim && active) ? Q.sim_order[t] : 0;
+        const int64_t *nrow = sim ? (E.nn + (isim - E.nn_row0) * E.mp1 + 1) : (Q.nn_star + (active ? t : 0) * Q.m_pred);
 
         // ---- gather: local row CAP-1 = the prediction point, rows CAP-1-m_pred .. CAP-2 = neighbours ----
         double rhs[S];
@@ -85,7 +95,7 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_krige_kern
                 dg = Q.prior;
 #pragma unroll
                 for (int l = 0; l < D; ++l)
-                    cx[l] = Q.locs_star[t * D + l] * E.inv_rho[l];
+                    cx[l] = (sim ? E.rec[isim * E.rs + l] : Q.locs_star[t * D + l]) * E.inv_rho[l];
             } else if (active && col >= 0 && col < Q.m_pred) {
                 const int64_t idx = nrow[col];
                 if (idx >= 0) {
@@ -208,11 +218,22 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_krige_kern
         constexpr int oe = Geo::lane_of(CAP - 1);
         if (active && lg == oe) {
             // Schur complement of the prediction point and minus the conditional mean of its residual
-            Q.var[t] = bad ? __longlong_as_double(0x7ff8000000000000ll) : Kr[se][CAP - 1];
-            Q.mean_resid[t] = -rhs[se];
+            const double var = bad ? __longlong_as_double(0x7ff8000000000000ll) : Kr[se][CAP - 1];
+            if (sim) {
+                const double *r = E.rec + isim * E.rs;
+                double yv = -rhs[se];
+                for (int b = 0; b < E.p; ++b)
+                    yv = fma(r[D + 1 + b], Q.beta[b], yv);
+                yv = fma(sqrt(fmax(var, 0.0)), Q.xi[isim], yv); // NaN variance (failed factorization) propagates
+                Q.rec_w[isim * E.rs + D] = yv;
+                Q.sim_y[isim] = yv;
+            } else {
+                Q.var[t] = var;
+                Q.mean_resid[t] = -rhs[se];
+            }
         }
         if (active && bad && lg == 0)
-            report_failure(E, t, 1);
+            report_failure(E, sim ? isim : t, 1);
         __syncwarp();
     }
 }

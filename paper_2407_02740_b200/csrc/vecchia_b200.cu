@@ -842,6 +842,95 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
     return VB200_OK;
 }
 
+// Conditional simulation from the neighbour-conditioned model (see include/vecchia_b200.h).
+extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta, int q, const double *beta,
+                              const double *xi, const int64_t *order, const int64_t *level_ptr, int64_t nlevels,
+                              double *y_out, int64_t *first_fail)
+{
+    if (!P)
+        return fail(VB200_EINVAL, "NULL problem");
+    if (!beta || !xi || !order || !level_ptr || !y_out)
+        return fail(VB200_EINVAL, "NULL argument");
+    if (P->nn_row0 != 0 || P->nn_rows != P->n)
+        return fail(VB200_EINVAL, "simulation needs the neighbour rows of every observation (not a shard)");
+    if (nlevels < 0 || (nlevels > 0 && (level_ptr[0] != 0 || level_ptr[nlevels] != P->n)))
+        return fail(VB200_EINVAL, "level_ptr must run from 0 to n");
+    CUDA_TRY(cudaSetDevice(P->device));
+    EvalParams E;
+    int rc = fill_params(P, family, theta, q, 0.0, 0, 0, E);
+    if (rc)
+        return rc;
+    if (first_fail)
+        *first_fail = -1;
+    if (P->n == 0)
+        return VB200_OK;
+    const int m_pred = P->mp1 - 1;
+    if (m_pred < 1)
+        return fail(VB200_EINVAL, "simulation needs at least one neighbour column");
+    const KrigeInstance *inst = krige_find(family, m_pred, P->d);
+    if (!inst)
+        return fail(VB200_EUNSUPPORTED, "no kriging kernel for this family / dimension / m (d in {2,3}, m <= 62)");
+    E.pair_tab = tiled_pair_table(inst->g, inst->s);
+    if (!E.pair_tab)
+        return fail(VB200_ECUDA, "pair table allocation failed");
+    KrigeParams K;
+    memset(&K, 0, sizeof(K));
+    K.m_pred = m_pred;
+    K.prior = theta[0] * (1.0 + theta[q - 1]);
+    for (int b = 0; b < P->p; ++b)
+        K.beta[b] = beta[b];
+    const size_t nb = sizeof(double) * (size_t)P->n;
+    double *d_xi = nullptr, *d_y = nullptr;
+    int64_t *d_order = nullptr;
+    CUDA_TRY(cudaMallocAsync(&d_xi, nb, P->stream));
+    CUDA_TRY(cudaMallocAsync(&d_y, nb, P->stream));
+    CUDA_TRY(cudaMallocAsync(&d_order, sizeof(int64_t) * (size_t)P->n, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_xi, xi, nb, cudaMemcpyDefault, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_order, order, sizeof(int64_t) * (size_t)P->n, cudaMemcpyDefault, P->stream));
+    K.xi = d_xi;
+    K.sim_y = d_y;
+    K.rec_w = P->rec;
+    reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
+    const size_t smem = (size_t)inst->smem_doubles * sizeof(double);
+    if (smem > P->smem_optin)
+        return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
+    CUDA_TRY(cudaFuncSetAttribute(inst->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaFuncSetAttribute(inst->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inst->kernel, 32, smem));
+    if (per_sm < 1)
+        per_sm = 1;
+    const int opw = 32 / inst->g;
+    // one launch per dependency level: the observations of a level only read values of lower levels,
+    // written by earlier launches on the same stream
+    for (int64_t l = 0; l < nlevels; ++l) {
+        const int64_t cnt = level_ptr[l + 1] - level_ptr[l];
+        if (cnt <= 0)
+            continue;
+        K.npred = cnt;
+        K.sim_order = d_order + level_ptr[l];
+        const int64_t nbatch = (cnt + opw - 1) / opw;
+        int64_t blocks = (int64_t)P->sm_count * per_sm;
+        if (blocks > nbatch)
+            blocks = nbatch;
+        inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+    }
+    CUDA_TRY(cudaGetLastError());
+    P->last_kernel = inst->name;
+    P->last_launches = 1 + (int)nlevels;
+    if (int rc0 = ensure_host_fail(P))
+        return rc0;
+    CUDA_TRY(cudaMemcpyAsync(y_out, d_y, nb, cudaMemcpyDefault, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream));
+    cudaFreeAsync(d_xi, P->stream);
+    cudaFreeAsync(d_y, P->stream);
+    cudaFreeAsync(d_order, P->stream);
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    if (*P->h_fail != ~0ull && first_fail)
+        *first_fail = (int64_t)(*P->h_fail >> 16);
+    return VB200_OK;
+}
+
 extern "C" int vb200_last_launch_count(const vb200_problem *P) { return P ? P->last_launches : 0; }
 extern "C" const char *vb200_last_kernel_name(const vb200_problem *P) { return P ? P->last_kernel : ""; }
 

@@ -144,6 +144,8 @@ def host_library():
         lib.vbh_order_maxmin.restype = ctypes.c_int
         lib.vbh_order_maxmin.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ip]
         lib.vbh_max_threads.restype = ctypes.c_int
+        lib.vbh_dependency_levels.restype = ctypes.c_int64
+        lib.vbh_dependency_levels.argtypes = [ip, ctypes.c_int64, ctypes.c_int, ip, ip]
         _host = lib
     return _host
 
@@ -219,3 +221,20 @@ def find_nearest_training(work_train, work_star, m_pred: int, workers: int | Non
     if rc != 0:
         raise RuntimeError(f"neighbor query failed with code {rc}")
     return out
+
+
+def dependency_levels(nn: NeighborArray):
+    """Level schedule of the conditioning DAG: ``(order, level_ptr)`` with ``order[level_ptr[l]:level_ptr[l+1]]``
+    the observations of level ``l`` (level = 1 + max level of the row's neighbours; rows without neighbours
+    are level 0), ascending within a level.  Observations of one level are conditionally independent of each
+    other given the lower levels: the launch schedule of the device conditional simulator (``simulate``)."""
+    idx = np.ascontiguousarray(nn.idx, dtype=np.int64)
+    n, mp1 = idx.shape
+    order = np.empty(n, dtype=np.int64)
+    level_ptr = np.zeros(n + 1, dtype=np.int64)
+    ip = ctypes.POINTER(ctypes.c_int64)
+    nlev = host_library().vbh_dependency_levels(idx.ctypes.data_as(ip), n, mp1, order.ctypes.data_as(ip),
+                                                level_ptr.ctypes.data_as(ip))
+    if nlev < 0:
+        raise ValueError("neighbor table is not causal: a row lists an index that is not smaller than its own")
+    return order, level_ptr[:nlev + 1].copy()

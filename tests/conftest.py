@@ -59,3 +59,9 @@ def make_instance(seed, n, d, p, family="exponential_isotropic", theta=(1.5, 0.2
         X[:, 1:] = rng.normal(size=(n, p - 1))
     y = rng.normal(size=n) + np.sin(3.0 * locs[:, 0]) + X @ rng.normal(size=p)
     return y, X, locs, np.asarray(theta, dtype=np.float64)
+
+
+@pytest.fixture(scope="session")
+def simulate_cases():
+    return np.load(GOLDEN / "simulate_cases.npz")
+

@@ -20,6 +20,8 @@ Files written
   fit_cases.npz      full Fisher-scoring fits (theta_hat, trace, iterations, ...)
   config1.npz        BASELINE config 1 (n=10 000, m=30): y + reference results
   krige_cases.npz    nearest-neighbour kriging (predict.krige) means / sds, noisy and latent
+  simulate_cases.npz oracle.simulate_nn_gp draws (sequential conditional simulation), incl. ragged head,
+                     p = 2, anisotropic d = 3 and a zero-nugget case
 """
 from __future__ import annotations
 
@@ -273,9 +275,38 @@ def krige_cases():
     print("krige_cases.npz:", len(specs), "cases")
 
 
+def simulate_cases():
+    """oracle.simulate_nn_gp (oracle.py:102-140) on small seeded instances."""
+    specs = [("iso_d2_m10", "exponential_isotropic", 2, 1, 10, 600, [1.7, 0.15, 0.05]),
+             ("iso_d2_m30", "exponential_isotropic", 2, 1, 30, 900, [0.8, 0.3, 0.2]),
+             ("iso_d2_p2_m5", "exponential_isotropic", 2, 2, 5, 300, [1.2, 0.1, 0.0]),
+             ("aniso_d3_m12", "exponential_anisotropic", 3, 1, 12, 500, [2.0, 0.3, 0.15, 0.5, 0.1])]
+    out = {}
+    for k, (name, family, d, p, m, n, theta) in enumerate(specs):
+        rng = np.random.default_rng(4000 + k)
+        locs = rng.uniform(0.0, 1.0, (n, d))
+        X = np.ones((n, p))
+        if p > 1:
+            X[:, 1:] = rng.normal(size=(n, p - 1))
+        beta = rng.normal(size=p)
+        cov = CovarianceParameters(family, np.array(theta))
+        nn = find_ordered_neighbors(locs, m)
+        seed = 77 + k
+        y = oracle.simulate_nn_gp(cov, beta, locs, X, nn, seed)
+        out[f"{name}/locs"], out[f"{name}/X"], out[f"{name}/beta"] = locs, X, beta
+        out[f"{name}/theta"], out[f"{name}/family"], out[f"{name}/m"] = cov.theta, np.array(family), np.array(m)
+        out[f"{name}/seed"], out[f"{name}/y"], out[f"{name}/nn"] = np.array(seed), y, nn.idx
+    out["names"] = np.array([s[0] for s in specs])
+    np.savez_compressed(OUT / "simulate_cases.npz", **out)
+    print("simulate_cases.npz:", len(specs), "cases")
+
+
 if __name__ == "__main__":
     if "--krige-only" in sys.argv:
         krige_cases()
+        sys.exit(0)
+    if "--simulate-only" in sys.argv:
+        simulate_cases()
         sys.exit(0)
     engine_cases()
     failure_cases()
@@ -283,3 +314,4 @@ if __name__ == "__main__":
     fit_cases()
     config1()
     krige_cases()
+    simulate_cases()

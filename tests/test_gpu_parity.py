@@ -359,6 +359,56 @@ def test_kriging_extension_families_against_oracle(family, d, theta):
     assert vg.rmse(ps.mean, mean) < 1e-9
 
 
+# ---- conditional simulation: reference oracle.simulate_nn_gp -------------------
+@pytest.mark.parametrize("name", ["iso_d2_m10", "iso_d2_m30", "iso_d2_p2_m5", "aniso_d3_m12"])
+def test_simulation_matches_reference(simulate_cases, name):
+    """Device level-scheduled conditional simulation == the reference's sequential loop on the same PCG64 draws."""
+    z = simulate_cases
+    g = lambda k: z[f"{name}/{k}"]
+    cov = vg.CovarianceParameters(str(g("family")), g("theta"))
+    y = vg.simulate_nn_gp(cov, g("beta"), g("locs"), g("X"), vg.NeighborArray(g("nn")), int(g("seed")))
+    np.testing.assert_allclose(y, g("y"), rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("family,d,theta", [("matern15_isotropic", 2, [1.2, 0.1, 0.1]),
+                                            ("exponential_spacetime", 3, [1.3, 0.2, 0.5, 0.1]),
+                                            ("matern_isotropic", 2, [1.0, 0.2, 0.8, 0.05])])
+def test_simulation_extension_families_against_oracle(family, d, theta):
+    from oracle import numpy_families as nf
+    rng = np.random.default_rng(5)
+    n, m = 700, 20
+    locs = rng.uniform(0, 1, (n, d))
+    X = np.column_stack([np.ones(n), rng.normal(size=n)])
+    beta = np.array([0.4, -1.1])
+    nn = vg.find_ordered_neighbors(locs, m)
+    cov = vg.CovarianceParameters(family, theta)
+    y = vg.simulate_nn_gp(cov, beta, locs, X, nn, seed=31)
+    want = nf.simulate_nn_gp(family, np.asarray(theta), beta, vg.covariance_registry(family).prepare_locs(locs), X,
+                             nn.idx, 31)
+    np.testing.assert_allclose(y, want, rtol=1e-9, atol=1e-9)
+
+
+def test_simulation_at_scale_recovers_the_model():
+    """n = 2^18: the draw has the model's likelihood statistics -- the profiled gradient at the simulating
+    parameters is small against its standard error (Fisher information), and a full fit recovers theta."""
+    n, m = 1 << 18, 30
+    rng = np.random.default_rng(2)
+    locs = rng.uniform(0, 1, (n, 2))
+    nn = vg.find_ordered_neighbors(locs, m)
+    theta = np.array([1.5, 0.05, 0.1])
+    cov = vg.CovarianceParameters("matern15_isotropic", theta)
+    X = np.ones((n, 1))
+    y = vg.simulate_nn_gp(cov, [0.3], locs, X, nn, seed=9)
+    assert np.all(np.isfinite(y)) and abs(y.var() / (theta[0] * (1 + theta[2])) - 1.0) < 0.2
+    ds = vg.Dataset(y, X, locs)
+    ev = vg.evaluate(ds, nn, cov)
+    zscore = ev.grad / np.sqrt(np.diag(ev.info))
+    assert np.all(np.abs(zscore) < 5.0), zscore
+    res = vg.fit(ds, nn, vg.ModelSpec(vg.default_start(ds, "matern15_isotropic"), m))
+    assert res.converged
+    np.testing.assert_allclose(res.theta_hat.theta, theta, rtol=0.05)
+
+
 # ---- sharded (multi-rank) evaluation on the device: two ranks share this GPU, gloo all-reduce ------
 _SHARD_WORKER = r"""
 import os, sys

@@ -341,3 +341,39 @@ def test_combine_partials_world_size_2_gloo(tmp_path):
     outs = [p.communicate(timeout=240)[0] for p in procs]
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o
+
+
+def test_dependency_levels_match_definition_and_reject_acausal_tables():
+    """Level schedule of the device conditional simulator (host C++): level(i) = 1 + max level of the neighbours."""
+    rng = np.random.default_rng(12)
+    for n, m, d in ((1, 3, 2), (40, 60, 2), (2500, 9, 3)):
+        locs = rng.uniform(0, 1, (n, d))
+        nn = vg.find_ordered_neighbors(locs, m)
+        order, level_ptr = vg.dependency_levels(nn)
+        lev = np.zeros(n, dtype=np.int64)
+        for i in range(n):
+            r = nn.idx[i, 1:]
+            r = r[r >= 0]
+            if r.size:
+                lev[i] = lev[r].max() + 1
+        assert np.array_equal(order, np.lexsort((np.arange(n), lev)))
+        assert np.array_equal(np.diff(level_ptr), np.bincount(lev))
+        assert level_ptr[0] == 0 and level_ptr[-1] == n
+    bad = nn.idx.copy()
+    bad[5, 1] = 7  # row 5 conditions on a LATER observation
+    with pytest.raises(ValueError):
+        vg.dependency_levels(vg.NeighborArray(bad))
+
+
+def test_simulation_needs_the_device_and_validates_first():
+    locs = np.random.default_rng(0).uniform(0, 1, (50, 2))
+    nn = vg.find_ordered_neighbors(locs, 5)
+    cov = vg.CovarianceParameters("exponential_isotropic", [1.0, 0.2, 0.1])
+    with pytest.raises(ValueError):
+        vg.simulate_nn_gp(cov, [0.0, 1.0], locs, np.ones((50, 1)), nn, seed=1)  # beta / design mismatch
+    with pytest.raises(ValueError):
+        vg.simulate_nn_gp(cov, [0.0], locs[:40], np.ones((40, 1)), nn, seed=1)   # table / locations mismatch
+    if _cabi.device_count() == 0:
+        with pytest.raises(vg.DeviceUnavailable):
+            vg.simulate_nn_gp(cov, [0.0], locs, np.ones((50, 1)), nn, seed=1)
+

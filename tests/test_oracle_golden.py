@@ -191,3 +191,20 @@ def test_kriging_oracle_matches_reference(krige_cases, name):
     # the host neighbour query of the product selects the same rows in the same order
     from paper_2407_02740_b200.preprocess import find_nearest_training
     assert np.array_equal(find_nearest_training(work, ws, int(g("m_pred"))), nbrs)
+
+
+SIMULATE = ["iso_d2_m10", "iso_d2_m30", "iso_d2_p2_m5", "aniso_d3_m12"]
+
+
+@pytest.mark.parametrize("name", SIMULATE)
+def test_simulation_oracle_matches_reference(simulate_cases, name):
+    """oracle simulate_nn_gp == the unmodified reference's oracle.simulate_nn_gp (same PCG64 stream), and the
+    product's host neighbour search reproduces the reference's table for the case."""
+    import paper_2407_02740_b200 as vg
+    from oracle import numpy_families as nf
+    z = simulate_cases
+    g = lambda k: z[f"{name}/{k}"]
+    y = nf.simulate_nn_gp(str(g("family")), g("theta"), g("beta"), g("locs"), g("X"), g("nn"), int(g("seed")))
+    np.testing.assert_allclose(y, g("y"), rtol=1e-11, atol=1e-12)
+    assert np.array_equal(vg.find_ordered_neighbors(g("locs"), int(g("m"))).idx, g("nn"))
+
