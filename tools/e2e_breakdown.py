@@ -17,7 +17,7 @@ ds = vg.Dataset(hy.numpy(), hX.numpy(), hl.numpy()); table = vg.NeighborArray(hn
 print("views pinned?", torch.from_numpy(table.idx).is_pinned(), torch.from_numpy(ds.y).is_pinned())
 theta = np.array([1.0, 0.05, 0.1])
 def sync(): torch.cuda.synchronize()
-for chunks in (1, 8, 8, 1, 16, 4):
+for chunks in (1, 8, 8, 16, 16, 32, 32, 64, 8):
     sync(); t0 = time.perf_counter()
     prob = engine.DeviceProblem(ds, table, "matern15_isotropic", upload_chunks=chunks); t1 = time.perf_counter()
     tot = prob.totals(theta); t2 = time.perf_counter()
