@@ -377,3 +377,20 @@ def test_simulation_needs_the_device_and_validates_first():
         with pytest.raises(vg.DeviceUnavailable):
             vg.simulate_nn_gp(cov, [0.0], locs, np.ones((50, 1)), nn, seed=1)
 
+
+def test_row_owner_pair_schedule_covers_every_pair_once(tmp_path):
+    """PairSched<G,S> (csrc/kernel_tiled.cuh): the static (lane, step) -> pair mapping of the row-owner pair phase
+    covers each off-diagonal pair of every tier exactly once and never touches the padding column.  Host build of
+    the same header with nvcc (no GPU needed)."""
+    import shutil
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(nvcc).exists():
+        pytest.skip("nvcc unavailable")
+    exe = tmp_path / "check_pair_schedule"
+    src = ROOT / "tests" / "native" / "check_pair_schedule.cu"
+    subprocess.run([nvcc, "-std=c++17", "-O1", "-I", str(ROOT / "include"), "-I", str(ROOT / "paper_2407_02740_b200" / "csrc"),
+                    "-o", str(exe), str(src)], check=True, capture_output=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and "FAIL" not in out.stdout, out.stdout
+    assert out.stdout.count(" ok") == 8
+
