@@ -418,7 +418,7 @@ def main(argv=None):
     ap.add_argument("--p", type=int, default=1)
     ap.add_argument("--family", default="matern15_isotropic")
     ap.add_argument("--theta", type=float, nargs="+", default=[1.0, 0.05, 0.1])
-    ap.add_argument("--layout", default="auto", choices=("auto", "warp_smem", "tiled_reg", "thread_smem"))
+    ap.add_argument("--layout", default="auto", choices=("auto", "warp_smem", "tiled_reg", "thread_smem", "thread_local"))
     ap.add_argument("--ref-seconds", type=float, default=2.0, help="target CPU seconds per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

@@ -80,7 +80,9 @@ enum vb200_layout {
     VB200_LAYOUT_AUTO = 0,
     VB200_LAYOUT_WARP_SMEM = 1,   /* warp per observation, matrices in shared memory (any shape) */
     VB200_LAYOUT_TILED_REG = 2,   /* sub-warp lane groups, rows register-resident (m+1 <= 64) */
-    VB200_LAYOUT_THREAD_SMEM = 3  /* thread per observation, packed triangle in shared memory */
+    VB200_LAYOUT_THREAD_SMEM = 3, /* thread per observation (the paper's layout), packed triangle of K staged in
+                                   * shared memory; study arm only, m+1 <= 32, d <= 3, p <= 4 */
+    VB200_LAYOUT_THREAD_LOCAL = 4 /* thread per observation, every matrix thread-local (local memory), as GpGpU does */
 };
 
 typedef struct vb200_problem vb200_problem; /* opaque: device-resident inputs of one dataset shard */

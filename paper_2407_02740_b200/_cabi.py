@@ -13,7 +13,7 @@ from .errors import DeviceUnavailable
 
 VB200_OK, VB200_EINVAL, VB200_ECUDA, VB200_ENOMEM, VB200_EUNSUPPORTED = 0, -1, -2, -3, -4
 
-LAYOUTS = {"auto": 0, "warp_smem": 1, "tiled_reg": 2, "thread_smem": 3}
+LAYOUTS = {"auto": 0, "warp_smem": 1, "tiled_reg": 2, "thread_smem": 3, "thread_local": 4}
 LAYOUT_NAMES = {v: k for k, v in LAYOUTS.items()}
 
 _dp, _ip = POINTER(c_double), POINTER(c_int64)

@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "kernel_warp_smem.cuh"
+#include "kernel_thread.cuh"
 #include "tiled_host.cuh"
 
 // ---------------------------------------------------------------------------
@@ -332,7 +333,7 @@ extern "C" int vb200_set_layout(vb200_problem *P, int layout)
 {
     if (!P)
         return fail(VB200_EINVAL, "NULL problem");
-    if (layout < VB200_LAYOUT_AUTO || layout > VB200_LAYOUT_THREAD_SMEM)
+    if (layout < VB200_LAYOUT_AUTO || layout > VB200_LAYOUT_THREAD_LOCAL)
         return fail(VB200_EINVAL, "unknown layout");
     P->layout = layout;
     return VB200_OK;
@@ -506,6 +507,53 @@ static int launch_warp_smem(vb200_problem *P, EvalParams &E, int *nblocks)
     return VB200_OK;
 }
 
+template <bool SMEM_TRI>
+static ws_kernel_t thread_kernel_for(int family)
+{
+    switch (family) {
+    case VB200_EXP_ISO: return vecchia_thread_kernel<FAM_EXP_ISO, SMEM_TRI>;
+    case VB200_EXP_ANISO: return vecchia_thread_kernel<FAM_EXP_ANISO, SMEM_TRI>;
+    case VB200_EXP_SPACETIME: return vecchia_thread_kernel<FAM_EXP_SPACETIME, SMEM_TRI>;
+    case VB200_MATERN15: return vecchia_thread_kernel<FAM_MATERN15, SMEM_TRI>;
+    case VB200_MATERN: return vecchia_thread_kernel<FAM_MATERN, SMEM_TRI>;
+    default: return vecchia_thread_kernel<FAM_MATERN25, SMEM_TRI>;
+    }
+}
+
+// Launch the THREAD layouts (one thread per observation; study arm).  One partial row per THREAD.
+static int launch_thread(vb200_problem *P, EvalParams &E, bool smem_tri, int *nblocks)
+{
+    if (!thread_layout_supported(P->mp1, P->d, P->p, E.q))
+        return fail(VB200_EUNSUPPORTED, "THREAD layouts serve m+1 <= 32, d <= 3, p <= 4, at most 2 range parameters");
+    ws_kernel_t kern = smem_tri ? thread_kernel_for<true>(E.family) : thread_kernel_for<false>(E.family);
+    const int threads = smem_tri ? 32 : 128;
+    const size_t smem = smem_tri ? sizeof(double) * 32 * TH_TRI : 0;
+    if (smem > P->smem_optin)
+        return fail(VB200_EUNSUPPORTED, "THREAD_SMEM needs 132 KB of shared memory per warp");
+    if (smem)
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    if (per_sm < 1)
+        per_sm = 1;
+    const int64_t count = E.i1 - E.i0;
+    int64_t blocks = (int64_t)P->sm_count * per_sm;
+    const int64_t need = (count + threads - 1) / threads;
+    if (blocks > need)
+        blocks = need;
+    if (blocks < 1)
+        blocks = 1;
+    int rc = ensure_partials(P, (size_t)blocks * threads * E.L);
+    if (rc)
+        return rc;
+    E.partials = P->partials;
+    kern<<<(unsigned)blocks, threads, smem, P->stream>>>(E);
+    CUDA_TRY(cudaGetLastError());
+    *nblocks = (int)(blocks * threads);
+    P->last_kernel = smem_tri ? "vecchia_thread_kernel<smem triangle>" : "vecchia_thread_kernel<local memory>";
+    return VB200_OK;
+}
+
 static int resolve_layout(const vb200_problem *P, int family, int q)
 {
     int layout = P->layout;
@@ -557,7 +605,9 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
             if (rc)
                 return rc;
         } else {
-            return fail(VB200_EUNSUPPORTED, "THREAD_SMEM layout is not built in this version");
+            rc = launch_thread(P, E, layout == VB200_LAYOUT_THREAD_SMEM, &nblocks);
+            if (rc)
+                return rc;
         }
         P->last_launches++;
         if (P->timing)

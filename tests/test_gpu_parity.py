@@ -42,6 +42,9 @@ def layouts_for(prob, q):
     prob.set_layout("auto")
     if prob.layout_for(q) == "tiled_reg":
         out.append("tiled_reg")
+    # the thread-per-observation study arms (the paper's layout): m+1 <= 32, d <= 3, p <= 4, <= 2 range parameters
+    if prob.mp1 <= 32 and prob.d <= 3 and prob.p <= 4 and q - 2 <= 2:
+        out += ["thread_smem", "thread_local"]
     return out
 
 
@@ -208,6 +211,17 @@ def test_every_compiled_tiled_instance_against_oracle():
                 if m == cap - 2:  # the widest m of the tier must be served by exactly this instance
                     assert f"G={g},S={s_}," in prob.last_kernel_name, (prob.last_kernel_name, g, s_, m)
                 fields_close(got, want, p, q, 1e-9)
+
+
+def test_thread_layouts_reject_shapes_beyond_their_capacity():
+    """The thread-per-observation study arms refuse shapes beyond their compile-time capacity (no fallback)."""
+    y, X, locs, theta = make_instance(3, 400, 2, 1)
+    wide = vg.find_ordered_neighbors(locs, 40)
+    with DeviceProblem(vg.Dataset(y, X, locs), wide, "exponential_isotropic") as prob:
+        for layout in ("thread_smem", "thread_local"):
+            prob.set_layout(layout)
+            with pytest.raises(NotImplementedError):
+                prob.totals(theta)
 
 
 def test_shard_sums_equal_whole_and_empty_range():
