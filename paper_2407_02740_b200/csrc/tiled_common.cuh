@@ -1,5 +1,5 @@
 // tiled_common.cuh -- definitions shared by the TILED_REG kernels (likelihood: kernel_tiled.cuh,
-// kriging: kernel_krige.cuh): family traits, the pair-parallel pair terms of the kriging kernel, the
+// kernel_tiled_pt.cuh; kriging: kernel_krige.cuh): family traits, the pair-parallel pair terms, the
 // lane-group geometry (G lanes x S rows per lane, boustrophedon folding), the packed column store.
 #pragma once
 #include "common.cuh"
