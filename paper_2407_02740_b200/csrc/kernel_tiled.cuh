@@ -36,7 +36,8 @@
 #define TILED_WPB 1 // warps per block; > 1: the warps of a block pass the phases of a batch together (barriers)
 #endif
 #ifndef TILED_ABLATE
-#define TILED_ABLATE 0 // timing experiments only: bit 0 skips the pair phase, 1 factorization, 2 back-substitution, 3 sweeps, 4 gather loads
+#define TILED_ABLATE 0 // timing experiments only: bit 0 skips the pair phase, 1 factorization, 2 back-substitution, 3 sweeps, 4 gather loads,
+                       // 5 replaces exp by a product, 6 adds 320 independent DFMAs per batch
 #endif
 #ifndef TILED_PD
 #define TILED_PD 3 // broadcast loads in flight ahead of their FMAs in the factorization
@@ -71,7 +72,11 @@ __device__ __forceinline__ void pair_terms_r(const EvalParams &E, const double *
         const double e = fma(-x2, y * y, 1.0);
         const double g = x2 * y;
         const double x = fma(fma(e, 0.375, 0.5), g * e, g);
+#if (TILED_ABLATE & 32)
+        const double se = 1e-3 * x2; // timing experiment: no exp (11 FP64 + 6 integer instructions + 1 table load less)
+#else
         const double se = exp_neg(x, etab); // sigma^2 exp(-x)
+#endif
         if constexpr (FAM == FAM_EXP_ISO) {
             Kv = se;
             Dv[0] = se * x;                 // * 1/range
@@ -687,6 +692,25 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 }
             }
         }
+#if (TILED_ABLATE & 64)
+        { // timing experiment: +320 independent one-register-operand DFMAs per batch
+            double dz[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                dz[t] = ze + t;
+#pragma unroll
+            for (int it = 0; it < 40; ++it)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    dz[t] = fma(dz[t], 1.0000001, 1e-9);
+            double dsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                dsum += dz[t];
+            if (dsum == 1.2345)
+                acc[0] += dsum;
+        }
+#endif
         const double logdet = log(d_e);
         const bool emit = active && failpiv == 0;
         // every lane evaluates every term (they are a handful of flops each) and keeps the ones it
