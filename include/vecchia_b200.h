@@ -204,6 +204,10 @@ int vb200_last_kernel_ms(vb200_problem *prob, double *ms);
  * launch, *sustained = all launches / total time.  MEASURED_PEAKS.json has no FP64
  * entry, so bench.py measures the roofline denominator itself. */
 int vb200_measure_fp64_peak(int device, double seconds, double *burst_tflops, double *sustained_tflops);
+/* The same through the FP64 MMA instruction (mma.sync m8n8k4, SASS DMMA): it issues on the same FP64
+ * units and reaches their nominal rate, so bench.py takes max(DFMA, DMMA) as the roofline denominator
+ * and records both. */
+int vb200_measure_fp64_peak_mma(int device, double seconds, double *burst_tflops, double *sustained_tflops);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,7 @@ _SIGNATURES = {
     "vb200_enable_timing": (c_int, [c_void_p, c_int]),
     "vb200_last_kernel_ms": (c_int, [c_void_p, _dp]),
     "vb200_measure_fp64_peak": (c_int, [c_int, c_double, _dp, _dp]),
+    "vb200_measure_fp64_peak_mma": (c_int, [c_int, c_double, _dp, _dp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

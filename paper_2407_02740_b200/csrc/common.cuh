@@ -59,6 +59,7 @@ struct EvalParams {
     int ws_doubles;          // per-warp scratch doubles (warp_smem layout)
     const unsigned int *pair_tab; // tiled layout: off-diagonal pair table of the tier (device memory)
     int sm_count;            // SMs of the device (tiled layout: start stagger of the resident blocks)
+    unsigned long long *dbg_clocks; // experiments only (-DTILED_CLOCKS): per-phase cycle sums; nullptr otherwise
     MaternOrder mat[3];      // FAM_MATERN only: orders nu, nu + h, nu - h
 };
 

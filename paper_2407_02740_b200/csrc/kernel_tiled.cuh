@@ -48,6 +48,18 @@
 #ifndef TILED_RNI
 #define TILED_RNI 4 // independent pair evaluations in flight per lane (row-owner pair phase)
 #endif
+// experiment (-DTILED_CLOCKS): per-phase clock64 accounting, summed over warps into E.dbg_clocks[0..15]
+// (and per factorization step into [16..16+CAP)); read back with vb200_debug_clocks.
+#ifdef TILED_CLOCKS
+#define PHASE_MARK(k)                                                                                    \
+    do {                                                                                                 \
+        const long long _t = clock64();                                                                  \
+        phc[k] += _t - pht;                                                                              \
+        pht = _t;                                                                                        \
+    } while (0)
+#else
+#define PHASE_MARK(k) do { } while (0)
+#endif
 
 // exp table premultiplied by sigma^2 (every family's covariance is sigma^2 * exp(-.) * polynomial)
 // and range-derivative values WITHOUT their constant factor (1/range, 1/(3 range), 1/range_axis):
@@ -267,6 +279,15 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
     }
     const int64_t nbatch = (E.i1 - E.i0 + OPW - 1) / OPW;
     const int64_t stride = (int64_t)gridDim.x * TILED_WPB;
+#ifdef TILED_CLOCKS
+    long long phc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pht = clock64();
+#if TILED_CLOCKS > 1
+    long long stc[CAP];
+#pragma unroll
+    for (int t = 0; t < CAP; ++t)
+        stc[t] = 0;
+#endif
+#endif
     // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
     for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
         const int64_t batch = batch0 + warp;
@@ -322,6 +343,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         }
         const int pad = CAP - nlive; // identity rows at the front of the local frame
         phase_sync();
+        PHASE_MARK(0);
 
         // ---- pair terms, row-owner.  Slot pair (s0, s1) = (2h, 2h+1): rows a0 = 2hG + lg and
         //      a1 = (2h+2)G - 1 - lg, a0 + a1 = T for every lane.  Step t: pair (a1, t) while t < a1,
@@ -412,6 +434,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             });
         }
         phase_sync();
+        PHASE_MARK(1);
 
         // ---- square-root-free factorization K = Lt D Lt^T (Lt unit lower, D = diag(d)), right-looking,
         //      with the forward substitutions of y and X fused in.  The Cholesky factor of the reference
@@ -441,6 +464,20 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             __syncwarp();
             const double *col = KLs + Geo::colbase(j);
             const int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
+#ifdef TILED_HEAD_SHFL
+            // experiment: the head of column j straight from the owners' registers (shorter pivot chain,
+            // 2-3 double shuffles instead of one or two broadcast loads)
+            (void)col;
+            hd = __shfl_sync(FULLMASK, Kr[sj][j], oj, G);
+            {
+                const int j1 = j + 1, s1 = j1 / G, o1 = (s1 & 1) ? (G - 1 - j1 % G) : (j1 % G);
+                h1 = __shfl_sync(FULLMASK, Kr[s1][j], o1, G);
+            }
+            if (cs != j && j + 2 < CAP) {
+                const int j2 = j + 2, s2 = j2 / G, o2 = (s2 & 1) ? (G - 1 - j2 % G) : (j2 % G);
+                h2 = __shfl_sync(FULLMASK, Kr[s2][j], o2, G);
+            }
+#else
             if (cs == j) {
                 const double2 v = *reinterpret_cast<const double2 *>(col + j);
                 hd = v.x;
@@ -451,10 +488,15 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 h1 = v.x;
                 h2 = v.y;
             }
+#endif
             failpiv = (failpiv == 0 && hd <= E.piv_floor) ? (j + 1) : failpiv;
         };
         auto multipliers = [&](const int j) { // Lo[s] = Lt[row][j] below the pivot row, exactly 0 for finished rows
+#if (TILED_ABLATE & 128)
+            const double rj = 2.0 - hd; // timing experiment: no reciprocal on the pivot chain (wrong numbers)
+#else
             const double rj = rcp_pos3(hd);
+#endif
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if ((s + 1) * G - 1 > j) {
@@ -530,6 +572,14 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             }
             if constexpr (j + 1 < CAP - 1)
                 multipliers(j + 1);
+#if defined(TILED_CLOCKS) && TILED_CLOCKS > 1
+            {
+                const long long _t = clock64();
+                stc[j] += _t - pht;
+                phc[2] += _t - pht;
+                pht = _t;
+            }
+#endif
         });
         // last pivot d_e (row CAP-1 = the observation itself): nothing left to update
         constexpr int se = S - 1;
@@ -546,6 +596,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      (a, l) of the symmetric D_r lives at colbase(a) + l (a < l) or colbase(l) + a (a >= l;
         //      the diagonal holds zeros). ----
         phase_sync();
+        PHASE_MARK(2);
         double sb[S], eb[S], rr[QD + 1][S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -607,6 +658,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         }
 
         phase_sync();
+        PHASE_MARK(3);
         // ---- [tt_1..tt_QD, ut] through Lt^-1 (unit-diagonal forward sweeps on the register-resident rows) ----
 #pragma unroll
         for (int j = 1; j < ((TILED_ABLATE & 8) ? 1 : CAP - 1); ++j) {
@@ -643,6 +695,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             return gsum(s0);
         };
         phase_sync();
+        PHASE_MARK(4);
         const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
         const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
         const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G) * rho_e;
@@ -732,7 +785,20 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 E.fail_rows[i - E.i0] = failpiv - pad;
         }
         phase_sync();
+        PHASE_MARK(5);
     }
+#ifdef TILED_CLOCKS
+    if (E.dbg_clocks != nullptr && lane == 0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            atomicAdd(E.dbg_clocks + t, (unsigned long long)phc[t]);
+#if TILED_CLOCKS > 1
+#pragma unroll
+        for (int t = 0; t < CAP; ++t)
+            atomicAdd(E.dbg_clocks + 16 + t, (unsigned long long)stc[t]);
+#endif
+    }
+#endif
 
     // ---- block partial: add the groups of this warp in fixed order, one row of `partials` per block ----
 #pragma unroll

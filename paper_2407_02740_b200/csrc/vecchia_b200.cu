@@ -111,6 +111,33 @@ __global__ void dfma_peak_kernel(double *sink, int iters, double a, double b)
         sink[0] = s;
 }
 
+// FP64 MMA (mma.sync m8n8k4, SASS DMMA.8x8x4) issue rate: eight independent accumulator tiles per warp.
+// Runs on the same FP64 units as DFMA; it reads fewer register operands per FMA and reaches the
+// nominal 64 FMA/clk/SM where three-operand DFMA streams do not (tools/micro/dmma_rate.cu).
+__global__ void dmma_peak_kernel(double *sink, int iters)
+{
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        c[i][0] = threadIdx.x;
+        c[i][1] = i;
+    }
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[i][0]), "+d"(c[i][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        s += c[i][0] + c[i][1];
+    if (s == 1.2345)
+        sink[0] = s;
+}
+
 // ---------------------------------------------------------------------------
 // problem object
 // ---------------------------------------------------------------------------
@@ -423,6 +450,25 @@ static MaternOrder matern_order(double nu)
     return M;
 }
 
+// experiments only: per-phase cycle counters of kernels built with -DTILED_CLOCKS (nullptr unless
+// vb200_debug_clocks has been called once to allocate them)
+static unsigned long long *g_dbg_clocks = nullptr;
+#define VB_DBG_CLOCKS 160
+extern "C" int vb200_debug_clocks(unsigned long long *out, int n, int reset)
+{
+    if (!g_dbg_clocks) {
+        CUDA_TRY(cudaMalloc(&g_dbg_clocks, sizeof(unsigned long long) * VB_DBG_CLOCKS));
+        CUDA_TRY(cudaMemset(g_dbg_clocks, 0, sizeof(unsigned long long) * VB_DBG_CLOCKS));
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (out && n > 0)
+        CUDA_TRY(cudaMemcpy(out, g_dbg_clocks, sizeof(unsigned long long) * (n < VB_DBG_CLOCKS ? n : VB_DBG_CLOCKS),
+                            cudaMemcpyDeviceToHost));
+    if (reset)
+        CUDA_TRY(cudaMemset(g_dbg_clocks, 0, sizeof(unsigned long long) * VB_DBG_CLOCKS));
+    return VB200_OK;
+}
+
 static int fill_params(const vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
                        int64_t i1, EvalParams &E)
 {
@@ -480,6 +526,7 @@ static int fill_params(const vb200_problem *P, int family, const double *theta, 
     }
     E.fail_word = P->fail_word;
     E.fail_count = P->fail_count;
+    E.dbg_clocks = g_dbg_clocks;
     if (family == VB200_MATERN) {
         const double nu0 = theta[2];
         if (!(nu0 > 2.0 * VB_MATERN_H) || nu0 > 60.0)
@@ -1053,6 +1100,49 @@ extern "C" int vb200_measure_fp64_peak(int device, double seconds, double *tflop
     while (elapsed < seconds) {
         CUDA_TRY(cudaEventRecord(e0));
         dfma_peak_kernel<<<blocks, threads>>>(sink, iters, 0.999999, 1e-9);
+        CUDA_TRY(cudaEventRecord(e1));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        elapsed += ms * 1e-3;
+        total_flops += flops_per_launch;
+        const double tf = flops_per_launch / (ms * 1e-3) * 1e-12;
+        if (tf > best)
+            best = tf;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    *tflops = best;
+    *sustained = total_flops / elapsed * 1e-12;
+    return VB200_OK;
+}
+
+// Best-of FP64 throughput of the DMMA micro-kernel (see dmma_peak_kernel).
+extern "C" int vb200_measure_fp64_peak_mma(int device, double seconds, double *tflops, double *sustained)
+{
+    if (!tflops || !sustained)
+        return fail(VB200_EINVAL, "output pointer is NULL");
+    if (vb200_device_count() <= device || device < 0)
+        return fail(VB200_ECUDA, "no such CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double *sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    const int threads = 256, blocks = sms * 2, iters = 8192;
+    const double flops_per_launch = (double)iters * 8 * (threads / 32) * (double)blocks * 2.0 * 8 * 8 * 4;
+    double best = 0.0, elapsed = 0.0, total_flops = 0.0;
+    dmma_peak_kernel<<<blocks, threads>>>(sink, 64); // warm-up
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (seconds <= 0.0)
+        seconds = 0.2;
+    while (elapsed < seconds) {
+        CUDA_TRY(cudaEventRecord(e0));
+        dmma_peak_kernel<<<blocks, threads>>>(sink, iters);
         CUDA_TRY(cudaEventRecord(e1));
         CUDA_TRY(cudaEventSynchronize(e1));
         float ms = 0.f;
