@@ -36,6 +36,7 @@ KERNEL_SPACETIME = 2
 KERNEL_MATERN15 = 3
 KERNEL_MATERN25 = 4
 KERNEL_MATERN = 5
+MATERN_NU_MIN, MATERN_NU_MAX = 2e-5, 60.0  # supported smoothness range of matern_isotropic
 MATERN_H = 1e-5  # smoothness central-difference step (csrc/common.cuh VB_MATERN_H)
 
 FAMILY_NAMES = (
@@ -198,4 +199,8 @@ def validate_parameters(params: CovarianceParameters, d: int) -> CovarianceFamil
         raise ValueError("variance and range parameters must be strictly positive")
     if th[-1] < 0.0:
         raise ValueError("nugget must be >= 0")
+    if fam.name == "matern_isotropic" and not (MATERN_NU_MIN < th[2] <= MATERN_NU_MAX):
+        # same bounds as the device library (csrc/vecchia_b200.cu fill_params): the smoothness derivative is
+        # a central difference of step MATERN_H, and x^nu K_nu(x) is evaluated by an upward recurrence in nu
+        raise ValueError(f"matern_isotropic: smoothness must lie in ({MATERN_NU_MIN}, {MATERN_NU_MAX}]")
     return fam

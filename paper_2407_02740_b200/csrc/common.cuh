@@ -60,6 +60,11 @@ struct EvalParams {
     const unsigned int *pair_tab; // tiled layout: off-diagonal pair table of the tier (device memory)
     int sm_count;            // SMs of the device (tiled layout: start stagger of the resident blocks)
     unsigned long long *dbg_clocks; // experiments only (-DTILED_CLOCKS): per-phase cycle sums; nullptr otherwise
+    // in-kernel finish (vb_finish below): the evaluation is ONE launch
+    double *out;             // result vector, L+2 doubles (totals, failure count, -(first failing index)-1)
+    double *group_sums;      // [ceil(gridDim.x / VB_FINISH_GROUP)][L]
+    unsigned int *tickets;   // [0]: groups done, [1 + g]: blocks of group g done; all zero between evaluations
+    unsigned long long *fail_latch; // copy of *fail_word of the finished evaluation (what the host reads)
     MaternOrder mat[3];      // FAM_MATERN only: orders nu, nu + h, nu - h
 };
 
@@ -363,6 +368,97 @@ __device__ __forceinline__ double warp_sum(double v)
     for (int off = 16; off > 0; off >>= 1)
         v += __shfl_xor_sync(0xffffffffu, v, off);
     return v;
+}
+
+// ---------------------------------------------------------------------------
+// In-kernel finish: the last block to arrive adds the partial rows in a FIXED order, so the totals do not
+// depend on scheduling (run-to-run bit-reproducible) and one evaluation is one launch (the reference
+// sums n-leading slot arrays on the host: engine/__init__.py:155-170).
+//   level 1: blocks are grouped VB_FINISH_GROUP at a time; the last block of a group to take its ticket adds the
+//            group's rows (index order, four interleaved accumulators) into group_sums[g];
+//   level 2: the last group to finish adds the group sums (index order) into out[0..L), publishes the
+//            failure word of this evaluation and resets tickets / failure word for the next one.
+// Every block calls this with ALL its threads after writing its `rpb` rows
+// partials[(blockIdx.x * rpb + k) * L + o].
+// ---------------------------------------------------------------------------
+#define VB_FINISH_GROUP 32
+#define VB_FINISH_MAXGROUPS 4096
+
+__device__ __forceinline__ double vb_fixed_sum(const double *base, const int rows, const size_t stride)
+{
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int r = 0;
+    for (; r + 4 <= rows; r += 4) {
+        s0 += __ldcg(base + (size_t)r * stride);
+        s1 += __ldcg(base + (size_t)(r + 1) * stride);
+        s2 += __ldcg(base + (size_t)(r + 2) * stride);
+        s3 += __ldcg(base + (size_t)(r + 3) * stride);
+    }
+    for (; r < rows; ++r)
+        s0 += __ldcg(base + (size_t)r * stride);
+    return (s0 + s1) + (s2 + s3);
+}
+
+struct FinishArgs { // the few fields of EvalParams vb_finish needs (by value: the callee is out of line)
+    const double *partials;
+    double *group_sums, *out;
+    unsigned int *tickets, *fail_count;
+    unsigned long long *fail_word, *fail_latch;
+    int L;
+};
+
+static __device__ __noinline__ void vb_finish_impl(const FinishArgs E, const int rpb)
+{
+    __shared__ unsigned int s_ticket;
+    const unsigned nb = gridDim.x, ng = (nb + VB_FINISH_GROUP - 1) / VB_FINISH_GROUP, grp = blockIdx.x / VB_FINISH_GROUP;
+    const unsigned gsize = min((unsigned)VB_FINISH_GROUP, nb - grp * VB_FINISH_GROUP);
+    const int L = E.L;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_ticket = atomicAdd(E.tickets + 1 + grp, 1u);
+    __syncthreads();
+    if (s_ticket != gsize - 1)
+        return;
+    __threadfence();
+    for (int o = threadIdx.x; o < L; o += blockDim.x)
+        E.group_sums[(size_t)grp * L + o] =
+            vb_fixed_sum(E.partials + (size_t)grp * VB_FINISH_GROUP * rpb * L + o, (int)gsize * rpb, (size_t)L);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_ticket = atomicAdd(E.tickets, 1u);
+    __syncthreads();
+    if (s_ticket != ng - 1)
+        return;
+    __threadfence();
+    for (int o = threadIdx.x; o < L; o += blockDim.x)
+        E.out[o] = vb_fixed_sum(E.group_sums + o, (int)ng, (size_t)L);
+    for (unsigned t = threadIdx.x; t < ng + 1; t += blockDim.x)
+        E.tickets[t] = 0u;
+    if (threadIdx.x == 0) {
+        const unsigned int cnt = *E.fail_count;
+        const unsigned long long w = *E.fail_word;
+        E.out[L] = (double)cnt;
+        E.out[L + 1] = cnt ? -(double)(w >> 16) - 1.0 : -INFINITY;
+        *E.fail_latch = w;
+        *E.fail_word = ~0ull;
+        *E.fail_count = 0u;
+    }
+}
+
+__device__ __forceinline__ void vb_finish(const EvalParams &E, const int rpb)
+{
+    FinishArgs F;
+    F.partials = E.partials;
+    F.group_sums = E.group_sums;
+    F.out = E.out;
+    F.tickets = E.tickets;
+    F.fail_count = E.fail_count;
+    F.fail_word = E.fail_word;
+    F.fail_latch = E.fail_latch;
+    F.L = E.L;
+    vb_finish_impl(F, rpb);
 }
 
 __device__ __forceinline__ void report_failure(const EvalParams &P, int64_t i, int pivot_plus1)

@@ -186,4 +186,5 @@ __global__ void __launch_bounds__(SMEM_TRI ? 32 : 128) vecchia_thread_kernel(con
     // one partial row per THREAD (the fixed-order reduction kernel adds them)
     for (int o = 0; o < A.L; ++o)
         P.partials[(size_t)tid * A.L + o] = acc[o];
+    vb_finish(P, (int)blockDim.x);
 }

@@ -36,14 +36,24 @@
 #define TILED_WPB 1 // warps per block; > 1: the warps of a block pass the phases of a batch together (barriers)
 #endif
 #ifndef TILED_ABLATE
-#define TILED_ABLATE 0 // timing experiments only: bit 0 skips the pair phase, 1 factorization, 2 back-substitution, 3 sweeps, 4 gather loads,
+#define TILED_ABLATE 0 // timing experiments only: bit 0 skips the pair phase, 1 factorization, 2 back-substitution, 3 sweeps,
                        // 5 replaces exp by a product, 6 adds 320 independent DFMAs per batch
 #endif
 #ifndef TILED_PD
-#define TILED_PD 3 // broadcast loads in flight ahead of their FMAs in the factorization
+#define TILED_PD 2 // broadcast loads in flight ahead of their FMAs in the factorization (2..5 measured within 2 %)
 #endif
 #ifndef TILED_STAGGER_NS
 #define TILED_STAGGER_NS 0 // experiment: start offset between the resident blocks of an SM (measured: no effect)
+#endif
+#ifndef TILED_PREFETCH
+#define TILED_PREFETCH 0 // 1: software-pipelined gather (next batch's indices / records requested one batch ahead);
+                         // measured slower at 12 warps per SM (registers), faster stand-alone: profiles/r2_experiments.md
+#endif
+#ifndef TILED_DD
+#define TILED_DD 2 // steps (of two columns) of D_r loads in flight ahead of the mat-vec FMAs
+#endif
+#ifndef TILED_BD
+#define TILED_BD 4 // column-store loads in flight ahead of the back-substitution chain
 #endif
 #ifndef TILED_RNI
 #define TILED_RNI 4 // independent pair evaluations in flight per lane (row-owner pair phase)
@@ -194,6 +204,45 @@ struct PairSched {
     }
 };
 
+// Element (a, l) of a packed symmetric matrix (lower triangle, columns back to back: (r, c), r >= c, at
+// colbase(c) + r) for a row a of slot s and a compile-time l.  Rows of slot s lie in [sG, (s+1)G): l beyond
+// the slot is always the column part (static offset from the lane's column base), l before it always the
+// row part (static offset from the row index); only inside the diagonal block does the side depend on the
+// lane.  `oz` is an opaque zero (see the kernel): it keeps the lane-dependent selects inside the batch loop.
+template <int G, int S, int s, int l>
+__device__ __forceinline__ double sym_packed_load(const double *M, const int colb_a, const int a, const int oz)
+{
+    using Geo = TileGeom<G, S>;
+    if constexpr (l >= (s + 1) * G)
+        return M[colb_a + l];
+    else if constexpr (l < s * G)
+        return M[Geo::colbase(l) + a];
+    else {
+        const int ao = a + oz;
+        return M[(ao < l) ? (colb_a + l) : (Geo::colbase(l) + ao)];
+    }
+}
+
+// rows a = rowi[s] of columns l0 = 2h, l0 + 1 of QD packed symmetric matrices, and the pair (u_l0, u_l0+1)
+template <int G, int S, int QD, int H, int s = 0>
+__device__ __forceinline__ void sym_fetch_pair(const double *Dms, const int DSZ, const double *us, const int (&colb_r)[S],
+                                               const int (&rowi)[S], const int oz, double (&dv)[2][QD][S], double2 &uv)
+{
+    constexpr int l0 = 2 * H, l1 = l0 + 1;
+    if constexpr (s == 0)
+        uv = *reinterpret_cast<const double2 *>(us + l0);
+    if constexpr (s < S) {
+#pragma unroll
+        for (int r = 0; r < QD; ++r) {
+            dv[0][r][s] = 0.0;
+            if constexpr (l0 >= 1)
+                dv[0][r][s] = sym_packed_load<G, S, s, l0>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+            dv[1][r][s] = sym_packed_load<G, S, s, l1>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+        }
+        sym_fetch_pair<G, S, QD, H, s + 1>(Dms, DSZ, us, colb_r, rowi, oz, dv, uv);
+    }
+}
+
 template <int G, int S, int D, int QD>
 struct LikSmem {
     using Geo = TileGeom<G, S>;
@@ -288,12 +337,55 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         stc[t] = 0;
 #endif
 #endif
+    // Software-pipelined gather: the neighbor indices of the NEXT batch are requested when the current
+    // batch enters its back-substitution, its point records when it enters the contraction (the rows of K
+    // are dead by then), so a batch starts with its inputs already in registers instead of waiting for an
+    // HBM read (indices) followed by a dependent L2 read (records): 2 900 cycles per batch before.
+    constexpr int RV = D + 1 + P; // values of a point record
+    int64_t nidx[S];
+    double nrec[S][RV];
+    auto load_idx = [&](const int64_t batch, int64_t (&idx)[S]) {
+        const int64_t i = E.i0 + batch * OPW + g;
+        const bool act = batch < nbatch && i < E.i1;
+        const int64_t *nrow = E.nn + (act ? (i - E.nn_row0) : 0) * E.mp1;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int col = CAP - 1 - rowi[s];
+            idx[s] = -1;
+            if (act && col < E.mp1)
+                idx[s] = nrow[col];
+        }
+    };
+    auto load_rec = [&](const int64_t (&idx)[S], double (&rv)[S][RV]) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+#pragma unroll
+            for (int t = 0; t < RV; ++t)
+                rv[s][t] = 0.0;
+            if (idx[s] >= 0) {
+                const double *r = E.rec + idx[s] * E.rs;
+#pragma unroll
+                for (int t = 0; t < RV; ++t)
+                    rv[s][t] = r[t];
+            }
+        }
+    };
+#if TILED_PREFETCH
+    load_idx((int64_t)blockIdx.x * TILED_WPB + warp, nidx);
+    load_rec(nidx, nrec);
+#endif
     // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
     for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
         const int64_t batch = batch0 + warp;
         const int64_t i = E.i0 + batch * OPW + g;
         const bool active = i < E.i1;
-        const int64_t *nrow = E.nn + (active ? (i - E.nn_row0) : 0) * E.mp1;
+#if !TILED_PREFETCH
+        load_idx(batch, nidx);
+        load_rec(nidx, nrec);
+#endif
+        // opaque zero, data-dependent in every iteration (indices are >= -1): blocks loop-invariant hoisting
+        // where it costs registers
+        const int oz = (int)((unsigned long long)(nidx[0] + 1) >> 63);
 
         // ---- gather: local index a <-> neighbor column CAP-1-a (observation last).  Coordinates are
         //      kept divided by the range of their axis.  Padding rows: diagonal 1, data 0, far away. ----
@@ -302,10 +394,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int a = rowi[s], col = CAP - 1 - a;
-            int64_t idx = -1;
-            if (active && col < E.mp1)
-                idx = (TILED_ABLATE & 16) ? (int64_t)((i * 7 + col * 13) % 1000) : nrow[col];
-            const bool live = idx >= 0;
+            (void)col;
+            const bool live = nidx[s] >= 0;
             double cx[DP];
 #pragma unroll
             for (int l = 0; l < DP; ++l)
@@ -316,14 +406,13 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             for (int b = 0; b < P; ++b)
                 rhs[1 + b][s] = 0.0;
             if (live) {
-                const double *r = E.rec + idx * E.rs;
 #pragma unroll
                 for (int l = 0; l < D; ++l)
-                    cx[l] = r[l] * E.inv_rho[l];
-                rhs[0][s] = r[D];
+                    cx[l] = nrec[s][l] * E.inv_rho[l];
+                rhs[0][s] = nrec[s][D];
 #pragma unroll
                 for (int b = 0; b < P; ++b)
-                    rhs[1 + b][s] = r[D + 1 + b];
+                    rhs[1 + b][s] = nrec[s][D + 1 + b];
             }
 #pragma unroll
             for (int l = 0; l < D; ++l)
@@ -444,11 +533,6 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      with LOOK-AHEAD: step j first updates column j+1 only, publishes it and starts the
         //      reciprocal of the next pivot, and only then applies column j to the rest of the trailing
         //      matrix, so the bulk of the rank-1 update fills the latency of the chain. ----
-        double invd[S]; // 1/d_a of the own rows
-#pragma unroll
-        for (int s = 0; s < S; ++s)
-            invd[s] = 1.0;
-        int failpiv = 0;
         // head of column j: pivot d_j and the next one or two entries.  Pairs (c0, c0+1) of a column are
         // read as one 128-bit broadcast load; cs(j) = first index of column j that starts an aligned pair.
         double Lo[S], xr[1 + P], hd, h1, h2 = 0.0;
@@ -489,7 +573,6 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 h2 = v.y;
             }
 #endif
-            failpiv = (failpiv == 0 && hd <= E.piv_floor) ? (j + 1) : failpiv;
         };
         auto multipliers = [&](const int j) { // Lo[s] = Lt[row][j] below the pivot row, exactly 0 for finished rows
 #if (TILED_ABLATE & 128)
@@ -500,14 +583,11 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if ((s + 1) * G - 1 > j) {
-                    const double Ls = Kr[s][j] * rj;
-                    Lo[s] = (rowi[s] > j) ? Ls : 0.0;
-                    Kr[s][j] = Ls;
+                    Lo[s] = (rowi[s] > j) ? Kr[s][j] * rj : 0.0;
+                    Kr[s][j] = Lo[s]; // the masked multiplier is what the forward sweeps below need
                 } else {
                     Lo[s] = 0.0;
                 }
-                if ((s + 1) * G - 1 >= j)
-                    invd[s] = (rowi[s] == j) ? rj : invd[s];
             }
         };
         if (!(TILED_ABLATE & 2)) {
@@ -585,9 +665,31 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         constexpr int se = S - 1;
         constexpr int oe = Geo::lane_of(CAP - 1);
         const double d_e = __shfl_sync(FULLMASK, Kr[se][CAP - 1], oe, G);
-        failpiv = (failpiv == 0 && d_e <= E.piv_floor) ? CAP : failpiv;
         const double rho_e = rcp_pos(d_e);
-        invd[se] = (rowi[se] == CAP - 1) ? rho_e : invd[se];
+        // 1/d_a of the own rows and the failure test, from the diagonal of the column store (the very
+        // values the pivot chain used, so the reciprocals are bit-identical to the chain's): keeps the
+        // per-step selects (owner-lane invd, running failure index) out of the factorization sweep.
+        __syncwarp();
+        double invd[S];
+        int failpiv = 0;
+        {
+            unsigned badm[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int a = rowi[s];
+                const double da = (a == CAP - 1) ? d_e : KLs[colb_r[s] + a];
+                const bool real = a >= 1;                       // local row 0: identity padding (store holds 0)
+                invd[s] = !real ? 1.0 : ((a == CAP - 1) ? rho_e : rcp_pos3(da));
+                badm[s] = __ballot_sync(FULLMASK, real && da <= E.piv_floor);
+                if (G < 32)
+                    badm[s] = (badm[s] >> (g * G)) & ((1u << (G & 31)) - 1u);
+            }
+            // lowest failing local row + 1 (slot s even: lane = row - sG, odd: lane = G-1 - (row - sG))
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s)
+                if (badm[s] != 0u)
+                    failpiv = s * G + ((s & 1) ? (G - 1 - (31 - __clz(badm[s]))) : (__ffs(badm[s]) - 1)) + 1;
+        }
 
         // ---- ut = Lt^-T e_last (u = ut / sqrt(d_e)): the lane owning index j accumulates
         //      sb_j = sum_{l>j} K(l,j) ut_l from the unscaled column store, ut_j = e_j - sb_j / d_j.  As
@@ -597,64 +699,106 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      the diagonal holds zeros). ----
         phase_sync();
         PHASE_MARK(2);
+#if TILED_PREFETCH
+        load_idx(batch + stride, nidx); // next batch of this warp (see the gather pipeline above)
+#endif
         double sb[S], eb[S], rr[QD + 1][S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             sb[s] = 0.0;
             eb[s] = (rowi[s] == CAP - 1) ? 1.0 : 0.0;
-#pragma unroll
-            for (int r = 0; r < QD; ++r)
-                rr[r][s] = 0.0;
         }
-        // the loads of step l-1 are issued before the shuffle of step l is waited for (they do not depend
-        // on ut), so the dependent chain of a step is one FMA + one shuffle
-        double Kc[S], Dc[QD][S];
-        auto fetch = [&](const int l, double (&Kl)[S], double (&Dl)[QD][S]) {
+        // The dependent chain of a step is one FMA + one shuffle; the column-store loads do not depend on
+        // ut and run TILED_BD steps ahead (few live registers here: the mat-vec D_r u is a separate pass
+        // below -- fused into this loop its loads were serialised behind the chain for lack of registers,
+        // 115 cycles per step measured, profiles/r2_experiments.md).  NO masks: a lane whose row a is not
+        // above l (a >= l) reads a finite, unrelated element of the store (colbase(a) + l stays inside it)
+        // and pollutes sb only at and after its own step l = a, when sb has already been consumed; every lane
+        // receives every ut_l, writes it to shared memory (same value, same address within a group) and
+        // reads its own entries back afterwards.
+        double *us = pts; // CAP doubles: ut (the coordinate table is dead by now)
+        {
+            constexpr int BD = TILED_BD;
+            double Kq[BD][S];
+            auto fetchK = [&](const int l, double (&Kl)[S]) {
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const bool above = rowi[s] < l;
-                Kl[s] = 0.0;
-                if (s * G < l) // slot has rows < l
-                    Kl[s] = above ? KLs[colb_r[s] + l] : 0.0;
-                const int addr = above ? (colb_r[s] + l) : (Geo::colbase(l) + rowi[s]);
+                for (int s = 0; s < S; ++s)
+                    if (s * G < l) // slot has rows < l
+                        Kl[s] = KLs[colb_r[s] + l];
+            };
+            if (lg == 0)
+                us[0] = 0.0;
+            if (!(TILED_ABLATE & 4)) {
+                static_for<0, BD>([&](auto ic) {
+                    constexpr int l = CAP - 1 - decltype(ic)::value;
+                    if constexpr (l >= 1)
+                        fetchK(l, Kq[decltype(ic)::value % BD]);
+                });
+                static_for<0, CAP - 1>([&](auto ic) {
+                    constexpr int it = decltype(ic)::value, l = CAP - 1 - it;
+                    constexpr int sl = l / G, ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
+                    const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
+                    us[l] = ul;
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+                        if (s * G < l)
+                            sb[s] = fma(Kq[it % BD][s], ul, sb[s]);
+                    if constexpr (l - BD >= 1)
+                        fetchK(l - BD, Kq[it % BD]);
+                });
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) // padding rows: ut = 0 whatever was read
+            rr[QD][s] = (rowi[s] < pad) ? 0.0 : us[rowi[s]];
+        // ---- tt_r = D_r ut: ut goes through shared memory (the coordinate table is dead by now), every lane
+        //      reads it back as broadcast pairs and walks its own rows of the packed symmetric D_r:
+        //      element (a, l) at colbase(a) + l (a < l) or colbase(l) + a (a >= l; diagonal and column 0 hold
+        //      zeros).  No dependent chain: two accumulators per row and matrix. ----
+        {
+            double t0[QD][S], t1[QD][S];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
-                    Dl[r][s] = Dms[r * DSZ + addr];
-            }
-        };
-        fetch(CAP - 1, Kc, Dc);
-        if (!(TILED_ABLATE & 4))
-        static_for<0, CAP - 1>([&](auto ic) {
-            constexpr int l = CAP - 1 - decltype(ic)::value;
-            constexpr int sl = l / G, ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
-            double Kn[S], Dn[QD][S];
-            if constexpr (l > 1)
-                fetch(l - 1, Kn, Dn);
-            const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
+                    t0[r][s] = t1[r][s] = 0.0;
+            // software pipeline: the loads of step h + DD are issued before the FMAs of step h (left to itself
+            // the compiler, short of registers here, issues each load right before its use: 30 cycles each)
+            constexpr int DD = TILED_DD, NH = CAP / 2;
+            double dq[DD][2][QD][S];
+            double2 uq[DD];
+            static_for<0, DD>([&](auto hc) {
+                constexpr int h = decltype(hc)::value;
+                if constexpr (h < NH)
+                    sym_fetch_pair<G, S, QD, h>(Dms, DSZ, us, colb_r, rowi, oz, dq[h % DD], uq[h % DD]);
+            });
+            static_for<0, NH>([&](auto hc) {
+                constexpr int h = decltype(hc)::value;
+                double dv[2][QD][S];
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                if (s * G < l)
-                    sb[s] = fma(Kc[s], ul, sb[s]);
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int r = 0; r < QD; ++r) {
+                        dv[0][r][s] = dq[h % DD][0][r][s];
+                        dv[1][r][s] = dq[h % DD][1][r][s];
+                    }
+                const double2 uv = uq[h % DD];
+                if constexpr (h + DD < NH)
+                    sym_fetch_pair<G, S, QD, h + DD>(Dms, DSZ, us, colb_r, rowi, oz, dq[h % DD], uq[h % DD]);
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int r = 0; r < QD; ++r) {
+                        t0[r][s] = fma(dv[0][r][s], uv.x, t0[r][s]);
+                        t1[r][s] = fma(dv[1][r][s], uv.y, t1[r][s]);
+                    }
+            });
+#pragma unroll
+            for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int r = 0; r < QD; ++r)
-                    rr[r][s] = fma(Dc[r][s], ul, rr[r][s]);
-            }
-            if constexpr (l > 1) {
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    Kc[s] = Kn[s];
-#pragma unroll
-                    for (int r = 0; r < QD; ++r)
-                        Dc[r][s] = Dn[r][s];
-                }
-            }
-        });
-#pragma unroll
-        for (int s = 0; s < S; ++s) { // padding rows: ut = 0 whatever was read
-            rr[QD][s] = (rowi[s] < pad) ? 0.0 : fma(-sb[s], invd[s], eb[s]);
-#pragma unroll
-            for (int r = 0; r < QD; ++r)
-                rr[r][s] *= dscale[r];
+                    rr[r][s] = (t0[r][s] + t1[r][s]) * dscale[r];
         }
 
         phase_sync();
@@ -664,10 +808,10 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         for (int j = 1; j < ((TILED_ABLATE & 8) ? 1 : CAP - 1); ++j) {
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
-            double Lm[S];
+            double Lm[S]; // multipliers of column j, stored masked (exactly 0 for rows <= j) by the factorization
 #pragma unroll
             for (int s = 0; s < S; ++s)
-                Lm[s] = ((s + 1) * G - 1 > j && rowi[s] > j) ? Kr[s][j] : 0.0;
+                Lm[s] = ((s + 1) * G - 1 > j) ? Kr[s][j] : 0.0;
 #pragma unroll
             for (int r = 0; r < QD + 1; ++r) {
                 const double x = __shfl_sync(FULLMASK, rr[r][sj], oj, G);
@@ -696,6 +840,9 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         };
         phase_sync();
         PHASE_MARK(4);
+#if TILED_PREFETCH
+        load_rec(nidx, nrec);
+#endif
         const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
         const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
         const double w_e = __shfl_sync(FULLMASK, rr[QD][se], oe, G) * rho_e;
@@ -811,6 +958,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         if (g == 0 && o < L)
             E.partials[((size_t)blockIdx.x * TILED_WPB + warp) * L + o] = v;
     }
+    vb_finish(E, TILED_WPB);
 }
 
 #include "kernel_tiled_pt.cuh"

@@ -409,5 +409,6 @@ __global__ void __launch_bounds__(32, tiled_min_blocks(G, S)) vecchia_tiled_pt_k
         if (g == 0 && o < L)
             E.partials[(size_t)blockIdx.x * L + o] = v;
     }
+    vb_finish(E, 1);
 }
 

@@ -243,4 +243,5 @@ __global__ void __launch_bounds__(WS_WARPS_MAX * 32) vecchia_warp_smem_kernel(co
         }
         P.partials[(size_t)blockIdx.x * A.L + o] = s;
     }
+    vb_finish(P, 1);
 }

@@ -55,40 +55,26 @@ __global__ void pack_records_kernel(const double *y, const double *X, const doub
         r[t] = 0.0;
 }
 
-// Fixed-order reduction of the block partials: thread o adds column o of
-// partials[nblocks][L] as a pairwise tree over a power-of-two padded index range,
-// so the result does not depend on scheduling (run-to-run reproducible).
-__global__ void reduce_partials_kernel(const double *partials, int nblocks, int L, double *out,
-                                       const unsigned long long *fail_word, const unsigned int *fail_count)
+// The partial rows are added inside the main kernel (vb_finish, common.cuh): one launch per evaluation.
+// An evaluation over an empty range still has to produce its result vector:
+__global__ void empty_result_kernel(double *out, int L)
 {
-    extern __shared__ double red[];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int o = 0; o < L; ++o) {
-        double s = 0.0;
-        for (int b = tid; b < nblocks; b += nt)
-            s += partials[(size_t)b * L + o];
-        red[tid] = s;
-        __syncthreads();
-        for (int off = nt >> 1; off > 0; off >>= 1) {
-            if (tid < off)
-                red[tid] += red[tid + off];
-            __syncthreads();
-        }
-        if (tid == 0)
-            out[o] = red[0];
-        __syncthreads();
-    }
-    if (tid == 0) {
-        const unsigned int cnt = *fail_count;
-        out[L] = (double)cnt;
-        out[L + 1] = cnt ? -(double)((*fail_word) >> 16) - 1.0 : -INFINITY;
+    for (int o = threadIdx.x; o < L; o += blockDim.x)
+        out[o] = 0.0;
+    if (threadIdx.x == 0) {
+        out[L] = 0.0;
+        out[L + 1] = -INFINITY;
     }
 }
 
+// fail_word[0]: live failure word (atomicMin), [1]: live failure count (low 32 bits), [2]: latched word of the
+// last finished likelihood evaluation.  The likelihood kernels reset [0] and [1] themselves when they finish
+// (vb_finish); kriging / simulation reset them before their launch with this kernel.
 __global__ void reset_fail_kernel(unsigned long long *fail_word, unsigned int *fail_count)
 {
     *fail_word = ~0ull;
     *fail_count = 0u;
+    fail_word[2] = ~0ull;
 }
 
 // Register-resident DFMA chains: 16 independent accumulators per thread.
@@ -151,8 +137,9 @@ struct vb200_problem {
     int64_t nn_row0 = 0, nn_rows = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    double *partials = nullptr;
+    double *partials = nullptr; // block partial rows, followed by the group sums of vb_finish
     size_t partials_cap = 0; // doubles
+    unsigned int *tickets = nullptr; // VB_FINISH_MAXGROUPS + 1 counters, zero between evaluations
     double *d_out = nullptr; // L+2 (own result vector for vb200_eval)
     size_t d_out_cap = 0;
     unsigned long long *fail_word = nullptr;
@@ -360,8 +347,12 @@ extern "C" int vb200_create(int device, int64_t n, int p, int d, int mp1, const 
             TRY_OR_FREE(cudaMemcpyAsync(tn, nn, sizeof(int64_t) * (size_t)nn_rows * mp1, cudaMemcpyHostToDevice,
                                         P->stream));
     }
-    TRY_OR_FREE(vb_malloc_async(&P->fail_word, 2 * sizeof(unsigned long long), P->stream));
+    TRY_OR_FREE(vb_malloc_async(&P->fail_word, 4 * sizeof(unsigned long long), P->stream));
     P->fail_count = reinterpret_cast<unsigned int *>(P->fail_word + 1);
+    TRY_OR_FREE(vb_malloc_async(&P->tickets, (VB_FINISH_MAXGROUPS + 1) * sizeof(unsigned int), P->stream));
+    TRY_OR_FREE(cudaMemsetAsync(P->tickets, 0, (VB_FINISH_MAXGROUPS + 1) * sizeof(unsigned int), P->stream));
+    reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
+    TRY_OR_FREE(cudaGetLastError());
     cleanup_tmp();
     // host inputs may be released by the caller on return; adopted device inputs need no wait
     if (copied_from_host)
@@ -382,6 +373,7 @@ extern "C" int vb200_destroy(vb200_problem *P)
     if (P->partials) cudaFreeAsync(P->partials, P->stream);
     if (P->d_out) cudaFreeAsync(P->d_out, P->stream);
     if (P->fail_word) cudaFreeAsync(P->fail_word, P->stream);
+    if (P->tickets) cudaFreeAsync(P->tickets, P->stream);
     if (P->h_out) cudaFreeHost(P->h_out);
     if (P->h_fail) cudaFreeHost(P->h_fail);
     if (P->ev0) cudaEventDestroy(P->ev0);
@@ -526,6 +518,8 @@ static int fill_params(const vb200_problem *P, int family, const double *theta, 
     }
     E.fail_word = P->fail_word;
     E.fail_count = P->fail_count;
+    E.fail_latch = P->fail_word + 2;
+    E.tickets = P->tickets;
     E.dbg_clocks = g_dbg_clocks;
     if (family == VB200_MATERN) {
         const double nu0 = theta[2];
@@ -536,6 +530,14 @@ static int fill_params(const vb200_problem *P, int family, const double *theta, 
             E.mat[t] = matern_order(orders[t]);
     }
     return VB200_OK;
+}
+
+// room for `rows` partial rows of L doubles plus the group sums of vb_finish behind them
+static size_t partial_doubles(size_t rows, int rows_per_block, int L)
+{
+    const size_t blocks = (rows + rows_per_block - 1) / rows_per_block;
+    const size_t groups = (blocks + VB_FINISH_GROUP - 1) / VB_FINISH_GROUP;
+    return (rows + groups) * (size_t)L;
 }
 
 static int ensure_partials(vb200_problem *P, size_t doubles)
@@ -576,11 +578,9 @@ static int launch_warp_smem(vb200_problem *P, EvalParams &E, int *nblocks)
     if (smem > P->smem_optin)
         return fail(VB200_EUNSUPPORTED, "m+1 too wide for the shared-memory layout on this device");
     ws_kernel_t kern = ws_kernel_for(E.family);
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem));
-    if (per_sm < 1)
-        per_sm = 1;
+    if (int rc0 = kernel_blocks_per_sm((const void *)kern, warps * 32, smem, false, &per_sm))
+        return rc0 == -100 ? fail(VB200_ECUDA, std::string("launch setup: ") + cudaGetErrorString(cudaGetLastError())) : rc0;
     const int64_t count = E.i1 - E.i0;
     int64_t blocks = (int64_t)P->sm_count * per_sm;
     const int64_t need = (count + warps - 1) / warps;
@@ -588,10 +588,13 @@ static int launch_warp_smem(vb200_problem *P, EvalParams &E, int *nblocks)
         blocks = need;
     if (blocks < 1)
         blocks = 1;
-    int rc = ensure_partials(P, (size_t)blocks * E.L);
+    if ((blocks + VB_FINISH_GROUP - 1) / VB_FINISH_GROUP > VB_FINISH_MAXGROUPS)
+        return fail(VB200_EUNSUPPORTED, "grid too large for the in-kernel reduction");
+    int rc = ensure_partials(P, partial_doubles((size_t)blocks, 1, E.L));
     if (rc)
         return rc;
     E.partials = P->partials;
+    E.group_sums = P->partials + (size_t)blocks * E.L;
     kern<<<(unsigned)blocks, warps * 32, smem, P->stream>>>(E);
     CUDA_TRY(cudaGetLastError());
     *nblocks = (int)blocks;
@@ -622,12 +625,9 @@ static int launch_thread(vb200_problem *P, EvalParams &E, bool smem_tri, int *nb
     const size_t smem = smem_tri ? sizeof(double) * 32 * TH_TRI : 0;
     if (smem > P->smem_optin)
         return fail(VB200_EUNSUPPORTED, "THREAD_SMEM needs 132 KB of shared memory per warp");
-    if (smem)
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-    if (per_sm < 1)
-        per_sm = 1;
+    if (int rc0 = kernel_blocks_per_sm((const void *)kern, threads, smem, false, &per_sm))
+        return rc0 == -100 ? fail(VB200_ECUDA, std::string("launch setup: ") + cudaGetErrorString(cudaGetLastError())) : rc0;
     const int64_t count = E.i1 - E.i0;
     int64_t blocks = (int64_t)P->sm_count * per_sm;
     const int64_t need = (count + threads - 1) / threads;
@@ -635,10 +635,13 @@ static int launch_thread(vb200_problem *P, EvalParams &E, bool smem_tri, int *nb
         blocks = need;
     if (blocks < 1)
         blocks = 1;
-    int rc = ensure_partials(P, (size_t)blocks * threads * E.L);
+    if ((blocks + VB_FINISH_GROUP - 1) / VB_FINISH_GROUP > VB_FINISH_MAXGROUPS)
+        return fail(VB200_EUNSUPPORTED, "grid too large for the in-kernel reduction");
+    int rc = ensure_partials(P, partial_doubles((size_t)blocks * threads, threads, E.L));
     if (rc)
         return rc;
     E.partials = P->partials;
+    E.group_sums = P->partials + (size_t)blocks * threads * E.L;
     kern<<<(unsigned)blocks, threads, smem, P->stream>>>(E);
     CUDA_TRY(cudaGetLastError());
     *nblocks = (int)(blocks * threads);
@@ -673,9 +676,8 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
         return rc;
     E.rows = d_rows;
     E.fail_rows = d_fail_rows;
+    E.out = d_out;
     P->last_launches = 0;
-    reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
-    P->last_launches++;
     int nblocks = 0;
     if (i1 > i0) {
         const int layout = resolve_layout(P, family, q);
@@ -685,8 +687,9 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
             if (!tiled_supported(family, P->mp1, P->p, P->d, q))
                 return fail(VB200_EUNSUPPORTED, "TILED_REG layout does not support this shape");
             rc = launch_tiled(P->stream, P->sm_count, P->smem_optin, E, &nblocks, &P->last_kernel,
-                              [&](size_t doubles) -> double * {
-                                  return ensure_partials(P, doubles) == VB200_OK ? P->partials : nullptr;
+                              [&](size_t rows) -> double * {
+                                  return ensure_partials(P, partial_doubles(rows, 1, E.L)) == VB200_OK ? P->partials
+                                                                                                       : nullptr;
                               });
             if (rc == -100)
                 return fail(VB200_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -706,14 +709,11 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
             CUDA_TRY(cudaEventRecord(P->ev1, P->stream));
     } else {
         P->last_kernel = "";
+        empty_result_kernel<<<1, 64, 0, P->stream>>>(d_out, E.L);
+        CUDA_TRY(cudaGetLastError());
+        P->last_launches++;
     }
-    rc = ensure_partials(P, 1);
-    if (rc)
-        return rc;
-    reduce_partials_kernel<<<1, 256, 256 * sizeof(double), P->stream>>>(P->partials, nblocks, E.L, d_out,
-                                                                        P->fail_word, P->fail_count);
-    CUDA_TRY(cudaGetLastError());
-    P->last_launches++;
+    (void)nblocks;
     return VB200_OK;
 }
 
@@ -748,7 +748,7 @@ extern "C" int vb200_fail_info(vb200_problem *P, int64_t *first_fail, int32_t *p
     CUDA_TRY(cudaSetDevice(P->device));
     if (int rc0 = ensure_host_fail(P))
         return rc0;
-    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
     const unsigned long long w = *P->h_fail;
@@ -794,7 +794,7 @@ extern "C" int vb200_eval(vb200_problem *P, int family, const double *theta, int
     if (rc)
         return rc;
     CUDA_TRY(cudaMemcpyAsync(P->h_out, P->d_out, sizeof(double) * (L + 2), cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
     memcpy(out_sums, P->h_out, sizeof(double) * L);

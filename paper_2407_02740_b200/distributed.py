@@ -34,11 +34,15 @@ def combine_partials(vec, group=None):
     import torch.distributed as dist
 
     L = vec.shape[0] - 2
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if multi:
         dist.all_reduce(vec[:L + 1], op=dist.ReduceOp.SUM, group=group)
-        if float(vec[L]) > 0.0:
-            dist.all_reduce(vec[L + 1:], op=dist.ReduceOp.MAX, group=group)
-    host = vec.detach().to("cpu", torch.float64).numpy()
+    # ONE device-to-host copy (and one synchronisation) per evaluation; the branch on the summed failure
+    # count is taken on the host, identically on every rank
+    host = vec.detach().to("cpu", torch.float64).numpy().copy()
+    if multi and host[L] > 0.0:  # rare: somebody failed -- recover the lowest failing index
+        dist.all_reduce(vec[L + 1:], op=dist.ReduceOp.MAX, group=group)
+        host[L + 1] = float(vec[L + 1])
     first_fail = -1
     if host[L] > 0.0:
         first_fail = int(round(-host[L + 1] - 1.0))
