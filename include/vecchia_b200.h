@@ -198,6 +198,15 @@ int vb200_tiled_instance(int k, int *lanes_per_obs, int *rows_per_lane, int *cap
 int vb200_enable_timing(vb200_problem *prob, int on);
 int vb200_last_kernel_ms(vb200_problem *prob, double *ms);
 
+/* ---- housekeeping --------------------------------------------------------- */
+/* The library's stream-ordered allocations come from a private memory pool per device that keeps up to
+ * 2 GiB of freed memory cached (so re-creating a problem per step does not pay the driver's map/unmap);
+ * this returns the cached memory of `device` to the driver (synchronises the device). */
+int vb200_release_memory(int device);
+/* Number of evaluations since process start for which VB200_LAYOUT_AUTO found no TILED_REG instance and ran
+ * the shape-agnostic WARP_SMEM kernel instead (roughly 10x slower): 0 means every evaluation took the fast path. */
+unsigned long long vb200_fallback_count(void);
+
 /* ---- measurement helper -------------------------------------------------- */
 /* FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA) from a register-resident
  * DFMA micro-kernel timed with CUDA events for about `seconds`: *burst = best single

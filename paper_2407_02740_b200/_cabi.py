@@ -49,6 +49,8 @@ _SIGNATURES = {
     "vb200_last_kernel_ms": (c_int, [c_void_p, _dp]),
     "vb200_measure_fp64_peak": (c_int, [c_int, c_double, _dp, _dp]),
     "vb200_measure_fp64_peak_mma": (c_int, [c_int, c_double, _dp, _dp]),
+    "vb200_release_memory": (c_int, [c_int]),
+    "vb200_fallback_count": (ctypes.c_ulonglong, []),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

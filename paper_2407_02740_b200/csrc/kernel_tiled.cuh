@@ -32,6 +32,12 @@
 #include "tiled_common.cuh"
 #include <type_traits>
 
+// Experiment knobs (ablations, clock accounting, alternative schedules) are honoured only in builds made with
+// -DVB200_EXPERIMENTS (tools/build_variant.py); the product build always uses the defaults below.
+#if !defined(VB200_EXPERIMENTS) && (defined(TILED_ABLATE) || defined(TILED_STAGGER_NS) || defined(TILED_CLOCKS) || \
+                                    defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB))
+#error "TILED_* experiment knobs need -DVB200_EXPERIMENTS"
+#endif
 #ifndef TILED_WPB
 #define TILED_WPB 1 // warps per block; > 1: the warps of a block pass the phases of a batch together (barriers)
 #endif

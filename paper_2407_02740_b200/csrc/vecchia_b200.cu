@@ -8,6 +8,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernel_warp_smem.cuh"
@@ -203,13 +204,19 @@ extern "C" int vb200_device_count(void)
 // dataset; bench.py's end-to-end leg creates one per step) does not pay cuMemCreate / map again
 // (measured: 1.2-1.7 ms of host time per create at n = 2^20 with the default pool, which returns unused
 // memory to the driver at every synchronisation).
+static unsigned long long g_fallback_evals = 0; // see vb200_fallback_count
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+
 static cudaError_t vb_malloc_async(void **ptr, size_t bytes, cudaStream_t stream)
 {
-    static std::mutex mu;
-    static std::map<int, cudaMemPool_t> pools;
-    static const bool use_default = getenv("VB200_DEFAULT_POOL") != nullptr; // development knob (A/B of the pool)
+    std::mutex &mu = g_pool_mu;
+    std::map<int, cudaMemPool_t> &pools = g_pools;
+#ifdef VB200_EXPERIMENTS
+    static const bool use_default = getenv("VB200_DEFAULT_POOL") != nullptr; // A/B of the private pool
     if (use_default)
         return cudaMallocAsync(ptr, bytes, stream);
+#endif
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess)
@@ -228,7 +235,11 @@ static cudaError_t vb_malloc_async(void **ptr, size_t bytes, cudaStream_t stream
             e = cudaMemPoolCreate(&pool, &props);
             if (e != cudaSuccess)
                 return e;
-            unsigned long long keep = ~0ull;
+            // freed blocks stay cached up to this much (the e2e path re-creates a 0.3 GB problem per step);
+            // anything above goes back to the driver at the next synchronisation, so a long-lived process
+            // that shares the GPU with another allocator (PyTorch's) is not starved.  vb200_release_memory()
+            // returns the rest.
+            unsigned long long keep = 2ull << 30;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
             pools[dev] = pool;
         } else {
@@ -442,6 +453,7 @@ static MaternOrder matern_order(double nu)
     return M;
 }
 
+#ifdef VB200_EXPERIMENTS
 // experiments only: per-phase cycle counters of kernels built with -DTILED_CLOCKS (nullptr unless
 // vb200_debug_clocks has been called once to allocate them)
 static unsigned long long *g_dbg_clocks = nullptr;
@@ -460,6 +472,9 @@ extern "C" int vb200_debug_clocks(unsigned long long *out, int n, int reset)
         CUDA_TRY(cudaMemset(g_dbg_clocks, 0, sizeof(unsigned long long) * VB_DBG_CLOCKS));
     return VB200_OK;
 }
+#else
+static unsigned long long *const g_dbg_clocks = nullptr;
+#endif
 
 static int fill_params(const vb200_problem *P, int family, const double *theta, int q, double jitter, int64_t i0,
                        int64_t i1, EvalParams &E)
@@ -681,6 +696,8 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
     int nblocks = 0;
     if (i1 > i0) {
         const int layout = resolve_layout(P, family, q);
+        if (P->layout == VB200_LAYOUT_AUTO && layout == VB200_LAYOUT_WARP_SMEM)
+            ++g_fallback_evals;
         if (P->timing)
             CUDA_TRY(cudaEventRecord(P->ev0, P->stream));
         if (layout == VB200_LAYOUT_TILED_REG) {
@@ -826,12 +843,23 @@ extern "C" int vb200_eval_rows(vb200_problem *P, int family, const double *theta
         return VB200_OK;
     double *d_rows = nullptr, *d_tot = nullptr;
     int *d_fail = nullptr;
-    CUDA_TRY(cudaMalloc(&d_rows, sizeof(double) * cnt * L));
-    CUDA_TRY(cudaMalloc(&d_fail, sizeof(int) * cnt));
-    CUDA_TRY(cudaMalloc(&d_tot, sizeof(double) * (L + 2)));
-    cudaMemsetAsync(d_rows, 0, sizeof(double) * cnt * L, P->stream);
-    cudaMemsetAsync(d_fail, 0, sizeof(int) * cnt, P->stream);
-    int rc = enqueue_eval(P, family, theta, q, jitter, i0, i1, d_tot, d_rows, d_fail);
+    auto release = [&]() {
+        if (d_rows) cudaFreeAsync(d_rows, P->stream);
+        if (d_fail) cudaFreeAsync(d_fail, P->stream);
+        if (d_tot) cudaFreeAsync(d_tot, P->stream);
+    };
+    int rc = VB200_OK;
+    cudaError_t e = vb_malloc_async(&d_rows, sizeof(double) * cnt * L, P->stream);
+    if (e == cudaSuccess) e = vb_malloc_async(&d_fail, sizeof(int) * cnt, P->stream);
+    if (e == cudaSuccess) e = vb_malloc_async(&d_tot, sizeof(double) * (L + 2), P->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_rows, 0, sizeof(double) * cnt * L, P->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_fail, 0, sizeof(int) * cnt, P->stream);
+    if (e != cudaSuccess) {
+        release();
+        return fail(e == cudaErrorMemoryAllocation ? VB200_ENOMEM : VB200_ECUDA,
+                    std::string("eval_rows buffers: ") + cudaGetErrorString(e));
+    }
+    rc = enqueue_eval(P, family, theta, q, jitter, i0, i1, d_tot, d_rows, d_fail);
     if (rc == VB200_OK) {
         cudaError_t e1 = cudaMemcpyAsync(rows_host, d_rows, sizeof(double) * cnt * L, cudaMemcpyDeviceToHost, P->stream);
         cudaError_t e2 = cudaMemcpyAsync(fail_host, d_fail, sizeof(int) * cnt, cudaMemcpyDeviceToHost, P->stream);
@@ -840,9 +868,7 @@ extern "C" int vb200_eval_rows(vb200_problem *P, int family, const double *theta
             rc = fail(VB200_ECUDA, std::string("eval_rows copy: ") +
                                        cudaGetErrorString(e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3)));
     }
-    cudaFree(d_rows);
-    cudaFree(d_fail);
-    cudaFree(d_tot);
+    release();
     return rc;
 }
 
@@ -899,6 +925,21 @@ extern "C" int vb200_last_kernel_ms(vb200_problem *P, double *ms)
     return VB200_OK;
 }
 
+// stream-ordered temporaries that are released on EVERY exit path of a function (round 1 leaked them when a
+// CUDA call in the middle failed)
+struct AsyncFreeGuard {
+    cudaStream_t stream;
+    std::vector<void *> ptrs;
+    explicit AsyncFreeGuard(cudaStream_t s) : stream(s) {}
+    void add(void *p) { ptrs.push_back(p); }
+    ~AsyncFreeGuard()
+    {
+        for (void *p : ptrs)
+            if (p)
+                cudaFreeAsync(p, stream);
+    }
+};
+
 extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, int q, const double *beta,
                            const double *locs_star, const int64_t *nn_star, int64_t npred, int m_pred, int latent,
                            double *mean_resid, double *var, int64_t *first_fail)
@@ -933,11 +974,13 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
         K.beta[b] = beta[b];
     double *d_locs = nullptr, *d_out = nullptr;
     int64_t *d_nn = nullptr;
+    AsyncFreeGuard tmp(P->stream);
     const size_t lbytes = sizeof(double) * (size_t)npred * P->d, nbytes = sizeof(int64_t) * (size_t)npred * m_pred;
     if (is_device_ptr(locs_star)) {
         K.locs_star = locs_star;
     } else {
         CUDA_TRY(vb_malloc_async(&d_locs, lbytes, P->stream));
+        tmp.add(d_locs);
         CUDA_TRY(cudaMemcpyAsync(d_locs, locs_star, lbytes, cudaMemcpyHostToDevice, P->stream));
         K.locs_star = d_locs;
     }
@@ -945,10 +988,12 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
         K.nn_star = nn_star;
     } else {
         CUDA_TRY(vb_malloc_async(&d_nn, nbytes, P->stream));
+        tmp.add(d_nn);
         CUDA_TRY(cudaMemcpyAsync(d_nn, nn_star, nbytes, cudaMemcpyHostToDevice, P->stream));
         K.nn_star = d_nn;
     }
     CUDA_TRY(vb_malloc_async(&d_out, sizeof(double) * 2 * (size_t)npred, P->stream));
+    tmp.add(d_out);
     K.mean_resid = d_out;
     K.var = d_out + npred;
     reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
@@ -975,9 +1020,6 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
     CUDA_TRY(cudaMemcpyAsync(mean_resid, d_out, sizeof(double) * (size_t)npred, cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaMemcpyAsync(var, d_out + npred, sizeof(double) * (size_t)npred, cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream));
-    if (d_locs) cudaFreeAsync(d_locs, P->stream);
-    if (d_nn) cudaFreeAsync(d_nn, P->stream);
-    cudaFreeAsync(d_out, P->stream);
     CUDA_TRY(cudaStreamSynchronize(P->stream));
     if (*P->h_fail != ~0ull && first_fail)
         *first_fail = (int64_t)(*P->h_fail >> 16);
@@ -1024,9 +1066,13 @@ extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta,
     const size_t nb = sizeof(double) * (size_t)P->n;
     double *d_xi = nullptr, *d_y = nullptr;
     int64_t *d_order = nullptr;
+    AsyncFreeGuard tmp(P->stream);
     CUDA_TRY(vb_malloc_async(&d_xi, nb, P->stream));
+    tmp.add(d_xi);
     CUDA_TRY(vb_malloc_async(&d_y, nb, P->stream));
+    tmp.add(d_y);
     CUDA_TRY(vb_malloc_async(&d_order, sizeof(int64_t) * (size_t)P->n, P->stream));
+    tmp.add(d_order);
     CUDA_TRY(cudaMemcpyAsync(d_xi, xi, nb, cudaMemcpyDefault, P->stream));
     CUDA_TRY(cudaMemcpyAsync(d_order, order, sizeof(int64_t) * (size_t)P->n, cudaMemcpyDefault, P->stream));
     K.xi = d_xi;
@@ -1064,9 +1110,6 @@ extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta,
         return rc0;
     CUDA_TRY(cudaMemcpyAsync(y_out, d_y, nb, cudaMemcpyDefault, P->stream));
     CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word, sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream));
-    cudaFreeAsync(d_xi, P->stream);
-    cudaFreeAsync(d_y, P->stream);
-    cudaFreeAsync(d_order, P->stream);
     CUDA_TRY(cudaStreamSynchronize(P->stream));
     if (*P->h_fail != ~0ull && first_fail)
         *first_fail = (int64_t)(*P->h_fail >> 16);
@@ -1160,3 +1203,20 @@ extern "C" int vb200_measure_fp64_peak_mma(int device, double seconds, double *t
     *sustained = total_flops / elapsed * 1e-12;
     return VB200_OK;
 }
+
+// Return the cached (freed) device memory of the library's private pool on `device` to the driver.
+extern "C" int vb200_release_memory(int device)
+{
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    auto it = g_pools.find(device);
+    if (it == g_pools.end())
+        return VB200_OK;
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemPoolTrimTo(it->second, 0));
+    return VB200_OK;
+}
+
+// Evaluations (since process start) for which VB200_LAYOUT_AUTO had no TILED_REG instance and fell back to
+// the shape-agnostic WARP_SMEM kernel (an order of magnitude slower): lets callers notice the cliff.
+extern "C" unsigned long long vb200_fallback_count(void) { return g_fallback_evals; }

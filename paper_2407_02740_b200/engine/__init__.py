@@ -21,7 +21,6 @@ raises ``DeviceUnavailable``.
 from __future__ import annotations
 
 import ctypes
-from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,6 +31,7 @@ from ..errors import DeviceUnavailable, NotPositiveDefinite
 from ..model import CovarianceParameters, Dataset, normalize_backend
 from ..preprocess import NeighborArray
 
+_FALLBACK_WARNED: set = set()
 CAPACITY_TIERS = (8, 16, 32, 64)
 VB_MAX_Q = 22  # csrc/common.cuh VB_MAXQ
 CORES = ("cuda",)
@@ -152,6 +152,7 @@ class DeviceProblem:
                 host_nn = torch.from_numpy(np.ascontiguousarray(shard_rows))
                 self._nn = torch.empty((rows, self.mp1), dtype=torch.int64, device=self.device)
                 side = torch.cuda.Stream(device=self.device)
+                side.wait_stream(self._stream)  # the block just handed out may still be in use by earlier work
                 self._nn.record_stream(side)
                 cuts = np.linspace(0, rows, upload_chunks + 1).astype(np.int64)
                 with torch.cuda.stream(side):
@@ -199,6 +200,7 @@ class DeviceProblem:
 
     # -- configuration ----------------------------------------------------------
     def set_layout(self, layout: str):
+        self._layout_name = layout
         _cabi.check(self._lib.vb200_set_layout(self._h, _cabi.LAYOUTS[layout]), "vb200_set_layout")
 
     def layout_for(self, q: int) -> str:
@@ -242,7 +244,22 @@ class DeviceProblem:
     # -- evaluation ---------------------------------------------------------------
     def _theta(self, theta):
         th = np.ascontiguousarray(theta, dtype=np.float64).ravel()
+        self._warn_if_fallback(th.shape[0])
         return th, th.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+    def _warn_if_fallback(self, q: int):
+        """layout "auto" silently ran the shape-agnostic kernel in round 1 (about 10x slower): say so, once per
+        shape.  The library counts those evaluations as well (vb200_fallback_count)."""
+        key = (self.kernel_code, q, self.p, self.d, self.mp1)
+        if key in _FALLBACK_WARNED:
+            return
+        _FALLBACK_WARNED.add(key)
+        if self._lib.vb200_get_layout(self._h, self.kernel_code, q) == _cabi.LAYOUTS["warp_smem"] and \
+                getattr(self, "_layout_name", "auto") == "auto":
+            import warnings
+            warnings.warn(f"no register-tiled kernel instance for family={self.family_name}, d={self.d}, p={self.p}, "
+                          f"m+1={self.mp1}: falling back to the generic shared-memory kernel (roughly 10x slower)",
+                          RuntimeWarning, stacklevel=3)
 
     def totals(self, theta, jitter: float = 0.0, i0: int | None = None, i1: int | None = None) -> np.ndarray:
         """Flat totals (L,) over [i0, i1) of this shard; raises NotPositiveDefinite."""
@@ -352,33 +369,26 @@ class DeviceProblem:
 
 
 # ---------------------------------------------------------------------------
-# facade with a small device-problem cache (upload once per dataset, not per call)
+# facade.  `run` is STATELESS like the reference's (engine/__init__.py:196-248): every call uploads the
+# arrays it is given, so in-place edits of y / X / locs / nn between calls are always honoured (round 1
+# cached device copies keyed on host addresses; the advisor flagged the stale-data hazard).  Code that
+# evaluates the same dataset repeatedly -- `inference.fit`, bench.py -- holds an explicit DeviceProblem.
 # ---------------------------------------------------------------------------
-_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
-_CACHE_SLOTS = 2
-
-
 def clear_cache() -> None:
-    while _CACHE:
-        _, (prob, _keep) = _CACHE.popitem()
-        prob.close()
+    """Kept for API compatibility with round 1: there is no implicit device cache any more."""
 
 
-def _cached_problem(ds: Dataset, nn: NeighborArray, family: str) -> DeviceProblem:
-    prep = "sphere" if family == "exponential_sphere" else "raw"
-    key = (ds.y.ctypes.data, ds.X.ctypes.data, ds.locs.ctypes.data, nn.idx.ctypes.data, ds.n, ds.p, ds.d,
-           nn.idx.shape[1], prep, covariance_registry(family).kernel_code)
-    hit = _CACHE.get(key)
-    if hit is not None:
-        _CACHE.move_to_end(key)
-        return hit[0]
-    prob = DeviceProblem(ds, nn, family)
-    # keep the host arrays alive so their addresses cannot be recycled while cached
-    _CACHE[key] = (prob, (ds.y, ds.X, ds.locs, nn.idx))
-    while len(_CACHE) > _CACHE_SLOTS:
-        _, (old, _keep) = _CACHE.popitem(last=False)
-        old.close()
-    return prob
+def _validate_core(core):
+    """The reference reads its default core from VECCHIAGP_CORE (engine/__init__.py:52-60); here the only
+    core is "cuda", so the variable may be unset, empty or "cuda" -- anything else is an error, as an unknown
+    name is in the reference."""
+    import os
+    core = core or os.environ.get("VECCHIAGP_CORE") or "cuda"
+    if core in _REFERENCE_CORES:
+        raise ValueError(f"core {core!r} is a CPU core of the reference package; this package provides 'cuda' only")
+    if core != "cuda":
+        raise ValueError(f"unknown core {core!r}")
+    return core
 
 
 def run(ds: Dataset, nn: NeighborArray, cov: CovarianceParameters, backend: str = "task",
@@ -390,19 +400,15 @@ def run(ds: Dataset, nn: NeighborArray, cov: CovarianceParameters, backend: str 
     factorization fails; no jitter is added unless requested.
     """
     normalize_backend(backend)
-    core = core or "cuda"
-    if core in _REFERENCE_CORES:
-        raise ValueError(f"core {core!r} is a CPU core of the reference package; this package provides 'cuda' only")
-    if core != "cuda":
-        raise ValueError(f"unknown core {core!r}")
+    _validate_core(core)
     validate_parameters(cov, ds.d)
     mp1 = nn.idx.shape[1]
     if nn.idx.shape[0] != ds.n:
         raise ValueError(f"neighbor table has {nn.idx.shape[0]} rows for n={ds.n}")
     if capacity_tier is not None and capacity_tier < mp1:
         raise ValueError(f"capacity tier {capacity_tier} too small for m+1={mp1}")
-    prob = _cached_problem(ds, nn, cov.family)
-    return prob.run(cov, jitter=float(jitter))
+    with DeviceProblem(ds, nn, cov.family) as prob:
+        return prob.run(cov, jitter=float(jitter))
 
 
 def process_observation(i: int, ds: Dataset, nn: NeighborArray, cov: CovarianceParameters,
@@ -411,8 +417,8 @@ def process_observation(i: int, ds: Dataset, nn: NeighborArray, cov: CovarianceP
     if not 0 <= i < ds.n:
         raise IndexError(f"observation index {i} outside [0, {ds.n})")
     validate_parameters(cov, ds.d)
-    prob = _cached_problem(ds, nn, cov.family)
-    rows, flags = prob.rows_host(cov.theta, jitter, i, i + 1)
+    with DeviceProblem(ds, nn, cov.family, upload_chunks=1) as prob:
+        rows, flags = prob.rows_host(cov.theta, jitter, i, i + 1)
     if flags[0]:
         raise NotPositiveDefinite(pivot=int(flags[0]) - 1, observation=i)
     return parts_from_flat(rows[0], ds.p, cov.nparms)

@@ -73,3 +73,51 @@ def fit_from_dict(doc: dict) -> FitResult:
                      loglik_trace=list(doc["loglik_trace"]), fisher_info=np.asarray(doc["fisher_info"]),
                      iterations=int(doc["iterations"]), converged=bool(doc["converged"]),
                      phase_timings=dict(doc.get("phase_timings_ms", {})))
+
+
+# ---------------------------------------------------------------------------
+# the reference's text formats (io.py:35-126): CSV datasets with a header row (response column, covariate
+# columns, coordinate columns) and CSV neighbor tables, floats written with repr() so a round trip is exact
+# ---------------------------------------------------------------------------
+def write_csv_dataset(ds: Dataset, path, y_col: str = "y", x_prefix: str = "x", loc_prefix: str = "loc") -> None:
+    names = [y_col] + [f"{x_prefix}{j}" for j in range(ds.p)] + [f"{loc_prefix}{j}" for j in range(ds.d)]
+    with open(path, "w") as handle:
+        handle.write(",".join(names) + "\n")
+        for i in range(ds.n):
+            row = [ds.y[i], *ds.X[i], *ds.locs[i]]
+            handle.write(",".join(repr(float(v)) for v in row) + "\n")
+
+
+def read_csv_dataset(path, y_col: str = "y", x_cols=None, loc_cols=None, x_prefix: str = "x",
+                     loc_prefix: str = "loc") -> Dataset:
+    """Columns are selected by name; by default every column named `x<j>` is a covariate and every `loc<j>` a
+    coordinate (the layout write_csv_dataset produces).  A dataset without covariate columns gets an intercept."""
+    with open(path) as handle:
+        header = [h.strip() for h in handle.readline().rstrip("\n").split(",")]
+        rows = [line.rstrip("\n").split(",") for line in handle if line.strip()]
+    if y_col not in header:
+        raise ValueError(f"no response column {y_col!r} in {path}")
+    pick = lambda prefix: [h for h in header if h.startswith(prefix) and h[len(prefix):].isdigit()]
+    x_cols = list(x_cols) if x_cols is not None else pick(x_prefix)
+    loc_cols = list(loc_cols) if loc_cols is not None else pick(loc_prefix)
+    missing = [c for c in x_cols + loc_cols if c not in header]
+    if missing:
+        raise ValueError(f"columns {missing} not in {path}")
+    if not loc_cols:
+        raise ValueError("no coordinate columns")
+    col = {h: k for k, h in enumerate(header)}
+    data = np.array([[float(v) for v in r] for r in rows], dtype=np.float64).reshape(len(rows), len(header))
+    X = data[:, [col[c] for c in x_cols]] if x_cols else np.ones((len(rows), 1))
+    return Dataset(data[:, col[y_col]], X, data[:, [col[c] for c in loc_cols]])
+
+
+def write_neighbors_csv(nn: NeighborArray, path) -> None:
+    with open(path, "w") as handle:
+        for row in nn.idx:
+            handle.write(",".join(str(int(v)) for v in row) + "\n")
+
+
+def read_neighbors_csv(path) -> NeighborArray:
+    with open(path) as handle:
+        rows = [[int(v) for v in line.split(",")] for line in handle if line.strip()]
+    return NeighborArray(np.array(rows, dtype=np.int64))

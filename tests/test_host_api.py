@@ -394,3 +394,63 @@ def test_row_owner_pair_schedule_covers_every_pair_once(tmp_path):
     assert out.returncode == 0 and "FAIL" not in out.stdout, out.stdout
     assert out.stdout.count(" ok") == 8
 
+
+# ---- round 2: text formats, core selection, smoothness bounds ---------------------------------------
+def test_csv_round_trips_are_exact(tmp_path):
+    from paper_2407_02740_b200 import io
+    rng = np.random.default_rng(4)
+    ds = vg.Dataset(rng.normal(size=9), rng.normal(size=(9, 2)), rng.uniform(size=(9, 3)))
+    io.write_csv_dataset(ds, tmp_path / "d.csv")
+    back = io.read_csv_dataset(tmp_path / "d.csv")
+    assert np.array_equal(back.y, ds.y) and np.array_equal(back.X, ds.X) and np.array_equal(back.locs, ds.locs)
+    only_locs = io.read_csv_dataset(tmp_path / "d.csv", x_cols=[], loc_cols=["loc0", "loc1"])
+    assert only_locs.p == 1 and np.all(only_locs.X == 1.0) and only_locs.d == 2
+    nn = vg.find_ordered_neighbors(ds.locs, 4)
+    io.write_neighbors_csv(nn, tmp_path / "n.csv")
+    assert np.array_equal(io.read_neighbors_csv(tmp_path / "n.csv").idx, nn.idx)
+    with pytest.raises(ValueError):
+        io.read_csv_dataset(tmp_path / "d.csv", y_col="nope")
+
+
+def test_core_selection_follows_the_reference_env_variable(monkeypatch):
+    monkeypatch.delenv("VECCHIAGP_CORE", raising=False)
+    assert engine._validate_core(None) == "cuda"
+    monkeypatch.setenv("VECCHIAGP_CORE", "cuda")
+    assert engine._validate_core(None) == "cuda"
+    monkeypatch.setenv("VECCHIAGP_CORE", "compiled")
+    with pytest.raises(ValueError):
+        engine._validate_core(None)
+    assert engine._validate_core("cuda") == "cuda"   # an explicit argument wins over the environment
+    monkeypatch.setenv("VECCHIAGP_CORE", "bogus")
+    with pytest.raises(ValueError):
+        engine._validate_core(None)
+
+
+def test_matern_smoothness_bounds_are_checked_on_the_host():
+    ok = vg.CovarianceParameters("matern_isotropic", [1.0, 0.2, 1.5, 0.1])
+    assert vg.validate_parameters(ok, 2).name == "matern_isotropic"
+    for nu in (1e-6, 61.0):
+        with pytest.raises(ValueError):
+            vg.validate_parameters(vg.CovarianceParameters("matern_isotropic", [1.0, 0.2, nu, 0.1]), 2)
+
+
+def test_fit_treats_out_of_domain_proposals_as_rejected_trials():
+    """A Fisher step that leaves the parameter domain (ValueError from validation / the library) must be halved like a
+    failed factorization, not abort the fit (advisor finding, round 1)."""
+    calls = []
+
+    def evaluator(theta):
+        calls.append(np.array(theta))
+        if theta[0] > 3.0:
+            raise ValueError("out of domain")
+        ll = -float(np.sum((np.log(theta) - np.log([2.0, 0.5, 0.1])) ** 2))
+        grad = -2.0 * (np.log(theta) - np.log([2.0, 0.5, 0.1])) / theta
+        info = np.diag(0.05 / theta ** 2)   # far too small: the full step overshoots out of the domain
+        return inference.ProfiledEvaluation(ll, np.zeros(1), grad, info, np.eye(1))
+
+    ds = vg.Dataset(np.zeros(5), np.ones((5, 1)), np.arange(10.0).reshape(5, 2))
+    nn = vg.find_ordered_neighbors(ds.locs, 2)
+    model = vg.ModelSpec(covariance=vg.CovarianceParameters("exponential_isotropic", [1.0, 0.4, 0.2]), m=2)
+    res = inference.fit(ds, nn, model, evaluator=evaluator, max_iters=60)
+    assert any(c[0] > 3.0 for c in calls), "the test must actually propose an out-of-domain point"
+    assert res.loglik_trace[-1] > res.loglik_trace[0]
