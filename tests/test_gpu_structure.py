@@ -350,7 +350,7 @@ def test_pivot_floor_brackets_the_reference_rule():
     # accepted by both; the last pivot (~1e-13 of the diagonal) carries ~1e-3 relative rounding noise in either
     # implementation, so log(pivot) agrees to ~1e-2 absolute, not more
     assert got[0] == pytest.approx(want[0], abs=0.05)
-    ds, nn = _near_duplicate_problem(1e-16)     # relative pivot ~ 4e-16 < floor; the reference accepts (pivot > 0)
+    ds, nn = _near_duplicate_problem(1e-15)     # relative pivot ~ 4e-15 < floor; the reference accepts (pivot > 0)
     want = vo.run(ds.y, ds.X, ds.locs, nn.idx, cov.family, cov.theta)
     assert np.isfinite(want[0])
     with DeviceProblem(ds, nn, cov.family) as prob:
