@@ -55,6 +55,9 @@
 #define TILED_PREFETCH 0 // 1: software-pipelined gather (next batch's indices / records requested one batch ahead);
                          // measured slower at 12 warps per SM (registers), faster stand-alone: profiles/r2_experiments.md
 #endif
+#ifndef TILED_FUSE_DU
+#define TILED_FUSE_DU 1 // the mat-vec D_r u rides in the stalls of the back-substitution chain (0: separate pass; 4 % slower)
+#endif
 #ifndef TILED_DD
 #define TILED_DD 2 // steps (of two columns) of D_r loads in flight ahead of the mat-vec FMAs
 #endif
@@ -249,6 +252,19 @@ __device__ __forceinline__ void sym_fetch_pair(const double *Dms, const int DSZ,
     }
 }
 
+// rows a = rowi[s] of column l of QD packed symmetric matrices
+template <int G, int S, int QD, int l, int s = 0>
+__device__ __forceinline__ void sym_fetch_col(const double *Dms, const int DSZ, const int (&colb_r)[S], const int (&rowi)[S],
+                                              const int oz, double (&dv)[QD][S])
+{
+    if constexpr (s < S) {
+#pragma unroll
+        for (int r = 0; r < QD; ++r)
+            dv[r][s] = sym_packed_load<G, S, s, l>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+        sym_fetch_col<G, S, QD, l, s + 1>(Dms, DSZ, colb_r, rowi, oz, dv);
+    }
+}
+
 template <int G, int S, int D, int QD>
 struct LikSmem {
     using Geo = TileGeom<G, S>;
@@ -276,9 +292,17 @@ __device__ __forceinline__ void phase_sync()
         __syncwarp();
 }
 
-template <int G, int S, int FAM, int D, int P>
+// PT = false: row-owner pair phase (fully unrolled, K straight into registers) -- the narrow tiers.
+// PT = true : pair-TABLE pair phase -- a rolled loop over a device pair table (pairs dealt round-robin to the
+//             lanes, two in flight per lane), K staged in the packed triangle in shared memory and read back
+//             row-wise into registers.  Small code where the unrolled row-owner phase would be 60-80 steps long
+//             (CAP = 48 / 64) and cheap around an out-of-line call (general-order Matern: the Bessel routine).
+//             Pairs that touch a padding row are not evaluated at all (the table lists live pairs first).
+// Everything after the pair phase is shared.
+template <int G, int S, int FAM, int D, int P, bool PT = false>
 __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
 {
+    static_assert(!PT || TILED_WPB == 1, "the pair-table variant runs one warp per block");
     using Geo = TileGeom<G, S>;
     using FT = FamTraits<FAM, D>;
     constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
@@ -376,9 +400,11 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             }
         }
     };
-#if TILED_PREFETCH
+#if TILED_PREFETCH == 1
     load_idx((int64_t)blockIdx.x * TILED_WPB + warp, nidx);
     load_rec(nidx, nrec);
+#elif TILED_PREFETCH == 2
+    load_idx((int64_t)blockIdx.x * TILED_WPB + warp, nidx);
 #endif
     // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
     for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
@@ -388,6 +414,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #if !TILED_PREFETCH
         load_idx(batch, nidx);
         load_rec(nidx, nrec);
+#elif TILED_PREFETCH == 2
+        load_rec(nidx, nrec); // indices arrived one batch ago, the records were prefetched into L1 / L2
 #endif
         // opaque zero, data-dependent in every iteration (indices are >= -1): blocks loop-invariant hoisting
         // where it costs registers
@@ -406,7 +434,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #pragma unroll
             for (int l = 0; l < DP; ++l)
                 cx[l] = 0.0;
-            cx[0] = 1e30 * (double)(a + 1);
+            if constexpr (!PT)
+                cx[0] = 1e30 * (double)(a + 1); // far away: every pair term with a padding row underflows
             rhs[0][s] = 0.0;
 #pragma unroll
             for (int b = 0; b < P; ++b)
@@ -428,15 +457,29 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 *reinterpret_cast<double2 *>(pts + a * DP + l) = make_double2(cx[l], cx[l + 1]);
             // diagonal block of the slot: the diagonal entry, zeros above it (never used, must be finite)
             const double dg = live ? E.diag : 1.0;
+            if constexpr (PT) {
+                KLs[colb_r[s] + a] = dg;
+            } else {
 #pragma unroll
-            for (int c = s * G; c < (s + 1) * G; ++c)
-                Kr[s][c] = (c == a) ? dg : 0.0;
-            if (s > 0)
-                Kr[s][0] = 0.0; // column 0 belongs to the padding row 0
+                for (int c = s * G; c < (s + 1) * G; ++c)
+                    Kr[s][c] = (c == a) ? dg : 0.0;
+                if (s > 0)
+                    Kr[s][0] = 0.0; // column 0 belongs to the padding row 0
+            }
             const unsigned bal = __ballot_sync(FULLMASK, live);
             nlive += __popc((G == 32) ? bal : ((bal >> (g * G)) & ((1u << (G & 31)) - 1u)));
         }
         const int pad = CAP - nlive; // identity rows at the front of the local frame
+        // wide tiers: factorization steps whose column belongs to a padding row of EVERY observation of the warp
+        // are identity steps (multipliers ~1e-200) and skip their rank-1 update (a warp-uniform branch, only
+        // compiled into the first NSKIP steps; the m = 30 tier has none)
+        constexpr int NSKIP = (CAP >= 48) ? 16 : 0;
+        int pad_w = pad;
+        if constexpr (NSKIP > 0) {
+#pragma unroll
+            for (int off = G; off < 32; off <<= 1)
+                pad_w = min(pad_w, __shfl_xor_sync(FULLMASK, pad_w, off));
+        }
         phase_sync();
         PHASE_MARK(0);
 
@@ -447,7 +490,69 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      chains (the compiler interleaves them; one chain alone is ~25 dependent FP64
         //      instructions), then all stores -- because a store to D_r between two loads of the
         //      point table would serialise the chains (the compiler cannot prove they do not alias). ----
-        {
+        if constexpr (PT) {
+            // ---- pair-table pair phase.  The table lists the off-diagonal pairs (a > c) by DESCENDING c, so the
+            //      k(k-1)/2 pairs among the live points come first; the rest is zero-filled. ----
+            using TS = TileSmem<G, S, D, QD>;
+            constexpr int NI = TS::NI;
+            const int nlp = nlive * (nlive - 1) / 2;
+            unsigned nxt[NI];
+#pragma unroll
+            for (int h = 0; h < NI; ++h)
+                nxt[h] = E.pair_tab[lg + h * G];
+            for (int t0 = lg; t0 < nlp; t0 += NI * G) {
+                unsigned ent[NI];
+#pragma unroll
+                for (int h = 0; h < NI; ++h)
+                    ent[h] = nxt[h];
+                if (t0 + NI * G < TS::TPAD) { // prefetch the next entries (L1-resident table)
+#pragma unroll
+                    for (int h = 0; h < NI; ++h)
+                        nxt[h] = E.pair_tab[t0 + (NI + h) * G];
+                }
+                double Kv[NI], Dv[NI][QD];
+#pragma unroll
+                for (int h = 0; h < NI; ++h) {
+                    const double *pra = pts + (ent[h] >> 24) * DP;
+                    const double *prc = pts + ((ent[h] >> 16) & 255) * DP;
+                    double dl[D];
+#pragma unroll
+                    for (int l = 0; l < DP; l += 2) {
+                        const double2 va = *reinterpret_cast<const double2 *>(pra + l);
+                        const double2 vc = *reinterpret_cast<const double2 *>(prc + l);
+                        dl[l] = va.x - vc.x;
+                        if (l + 1 < D)
+                            dl[l + 1 < D ? l + 1 : l] = va.y - vc.y;
+                    }
+                    pair_terms_r<FAM, D>(E, etab, dl, Kv[h], Dv[h]);
+                }
+                // entries past nlp in the last iteration belong to padding pairs: written here, overwritten with
+                // zeros below (after the warp sync)
+#pragma unroll
+                for (int h = 0; h < NI; ++h) {
+                    const int kidx = ent[h] & 0xffff;
+                    KLs[kidx] = Kv[h];
+#pragma unroll
+                    for (int j = 0; j < QD; ++j)
+                        Dms[j * DSZ + kidx] = Dv[h][j];
+                }
+            }
+            __syncwarp();
+            for (int t = nlp + lg; t < TS::TOFF; t += G) {
+                const int kidx = E.pair_tab[t] & 0xffff;
+                KLs[kidx] = 0.0;
+#pragma unroll
+                for (int j = 0; j < QD; ++j)
+                    Dms[j * DSZ + kidx] = 0.0;
+            }
+            __syncwarp();
+            // own rows into registers (entries above the diagonal: finite, never used)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int c = 0; c < (s + 1) * G; ++c)
+                    Kr[s][c] = KLs[Geo::colbase(c) + rowi[s]];
+        } else {
             using PS = PairSched<G, S>;
             constexpr int NI = TILED_RNI;
             if (!(TILED_ABLATE & 1))
@@ -619,41 +724,46 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             constexpr int NPAIR = (CAP - cb0 + 1) / 2;
             constexpr int PD = TILED_PD;
             double2 ring[PD];
+            const bool work = (j >= NSKIP) || (j >= pad_w); // compile-time true beyond the first NSKIP steps
+            if (work) {
 #pragma unroll
-            for (int i = 0; i < PD; ++i)
-                if (i < NPAIR)
-                    ring[i] = *reinterpret_cast<const double2 *>(col + cb0 + 2 * i);
+                for (int i = 0; i < PD; ++i)
+                    if (i < NPAIR)
+                        ring[i] = *reinterpret_cast<const double2 *>(col + cb0 + 2 * i);
 #pragma unroll
-            for (int r = 0; r < 1 + P; ++r)
+                for (int r = 0; r < 1 + P; ++r)
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+                        if ((s + 1) * G - 1 > j)
+                            rhs[r][s] = fma(-Lc[s], xr[r], rhs[r][s]);
 #pragma unroll
                 for (int s = 0; s < S; ++s)
-                    if ((s + 1) * G - 1 > j)
-                        rhs[r][s] = fma(-Lc[s], xr[r], rhs[r][s]);
-#pragma unroll
-            for (int s = 0; s < S; ++s)
-                if ((s + 1) * G - 1 >= j + 1)
-                    Kr[s][j + 1] = fma(-Lc[s], h1, Kr[s][j + 1]);
+                    if ((s + 1) * G - 1 >= j + 1)
+                        Kr[s][j + 1] = fma(-Lc[s], h1, Kr[s][j + 1]);
+            }
             if constexpr (j + 1 < CAP - 1)
                 publish(j + 1);
             // the rest of the trailing update with column j
-            if constexpr (cs != j && j + 2 < CAP) {
+            if (work) {
+                if constexpr (cs != j && j + 2 < CAP) {
 #pragma unroll
-                for (int s = 0; s < S; ++s)
-                    if ((s + 1) * G - 1 >= j + 2)
-                        Kr[s][j + 2] = fma(-Lc[s], g2, Kr[s][j + 2]);
-            }
+                    for (int s = 0; s < S; ++s)
+                        if ((s + 1) * G - 1 >= j + 2)
+                            Kr[s][j + 2] = fma(-Lc[s], g2, Kr[s][j + 2]);
+                }
 #pragma unroll
-            for (int i = 0; i < NPAIR; ++i) {
-                const int c0 = cb0 + 2 * i;
-                const double2 v = ring[i % PD];
-                if (i + PD < NPAIR)
-                    ring[i % PD] = *reinterpret_cast<const double2 *>(col + c0 + 2 * PD);
+                for (int i = 0; i < NPAIR; ++i) {
+                    const int c0 = cb0 + 2 * i;
+                    const double2 v = ring[i % PD];
+                    if (i + PD < NPAIR)
+                        ring[i % PD] = *reinterpret_cast<const double2 *>(col + c0 + 2 * PD);
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if ((s + 1) * G - 1 >= c0)
-                        Kr[s][c0] = fma(-Lc[s], v.x, Kr[s][c0]);
-                    if (c0 + 1 < CAP && (s + 1) * G - 1 >= c0 + 1)
-                        Kr[s][c0 + 1] = fma(-Lc[s], v.y, Kr[s][c0 + 1]);
+                    for (int s = 0; s < S; ++s) {
+                        if ((s + 1) * G - 1 >= c0)
+                            Kr[s][c0] = fma(-Lc[s], v.x, Kr[s][c0]);
+                        if (c0 + 1 < CAP && (s + 1) * G - 1 >= c0 + 1)
+                            Kr[s][c0 + 1] = fma(-Lc[s], v.y, Kr[s][c0 + 1]);
+                    }
                 }
             }
             if constexpr (j + 1 < CAP - 1)
@@ -726,6 +836,15 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         {
             constexpr int BD = TILED_BD;
             double Kq[BD][S];
+#if TILED_FUSE_DU
+            // the mat-vec D_r ut rides in the stalls of the chain (its loads BD steps ahead as well)
+            double Dq[BD][QD][S];
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+#pragma unroll
+                for (int r = 0; r < QD; ++r)
+                    rr[r][s] = 0.0;
+#endif
             auto fetchK = [&](const int l, double (&Kl)[S]) {
 #pragma unroll
                 for (int s = 0; s < S; ++s)
@@ -737,8 +856,12 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             if (!(TILED_ABLATE & 4)) {
                 static_for<0, BD>([&](auto ic) {
                     constexpr int l = CAP - 1 - decltype(ic)::value;
-                    if constexpr (l >= 1)
+                    if constexpr (l >= 1) {
                         fetchK(l, Kq[decltype(ic)::value % BD]);
+#if TILED_FUSE_DU
+                        sym_fetch_col<G, S, QD, l>(Dms, DSZ, colb_r, rowi, oz, Dq[decltype(ic)::value % BD]);
+#endif
+                    }
                 });
                 static_for<0, CAP - 1>([&](auto ic) {
                     constexpr int it = decltype(ic)::value, l = CAP - 1 - it;
@@ -749,8 +872,19 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                     for (int s = 0; s < S; ++s)
                         if (s * G < l)
                             sb[s] = fma(Kq[it % BD][s], ul, sb[s]);
-                    if constexpr (l - BD >= 1)
+#if TILED_FUSE_DU
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+#pragma unroll
+                        for (int r = 0; r < QD; ++r)
+                            rr[r][s] = fma(Dq[it % BD][r][s], ul, rr[r][s]);
+#endif
+                    if constexpr (l - BD >= 1) {
                         fetchK(l - BD, Kq[it % BD]);
+#if TILED_FUSE_DU
+                        sym_fetch_col<G, S, QD, l - BD>(Dms, DSZ, colb_r, rowi, oz, Dq[it % BD]);
+#endif
+                    }
                 });
             }
             __syncwarp();
@@ -762,6 +896,13 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      reads it back as broadcast pairs and walks its own rows of the packed symmetric D_r:
         //      element (a, l) at colbase(a) + l (a < l) or colbase(l) + a (a >= l; diagonal and column 0 hold
         //      zeros).  No dependent chain: two accumulators per row and matrix. ----
+#if TILED_FUSE_DU
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int r = 0; r < QD; ++r)
+                rr[r][s] *= dscale[r];
+#else
         {
             double t0[QD][S], t1[QD][S];
 #pragma unroll
@@ -806,6 +947,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                 for (int r = 0; r < QD; ++r)
                     rr[r][s] = (t0[r][s] + t1[r][s]) * dscale[r];
         }
+#endif
 
         phase_sync();
         PHASE_MARK(3);
@@ -846,8 +988,13 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         };
         phase_sync();
         PHASE_MARK(4);
-#if TILED_PREFETCH
+#if TILED_PREFETCH == 1
         load_rec(nidx, nrec);
+#elif TILED_PREFETCH == 2
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (nidx[s] >= 0)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(E.rec + nidx[s] * E.rs));
 #endif
         const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
         const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
@@ -967,14 +1114,12 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
     vb_finish(E, TILED_WPB);
 }
 
-#include "kernel_tiled_pt.cuh"
-
 // ---------------------------------------------------------------------------
 // host side: instance table and launch
 // ---------------------------------------------------------------------------
 struct TiledInstance {
     int g, s, cap, family, d, p, wpb;
-    int pair_table; // 1: the pair-table variant (kernel_tiled_pt.cuh) -- needs EvalParams::pair_tab
+    int pair_table; // 1: the pair-table pair phase (PT = true) -- needs EvalParams::pair_tab
     void (*kernel)(const EvalParams);
     int smem_doubles;
     const char *name;
@@ -989,7 +1134,7 @@ struct TiledInstance {
 
 #define TILED_INST_PT(G_, S_, FAM_, D_, P_)                                                                     \
     {                                                                                                           \
-        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, 1, vecchia_tiled_pt_kernel<G_, S_, FAM_, D_, P_>,                         \
-            TileSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
-            "vecchia_tiled_pt_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                         \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, 1, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_, true>,              \
+            LikSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
+            "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ",pair-table>"               \
     }

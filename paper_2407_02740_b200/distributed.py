@@ -24,6 +24,9 @@ def shard_bounds(n: int, world_size: int, rank: int) -> tuple:
     return i0, i0 + base + (1 if rank < extra else 0)
 
 
+_PINNED: dict = {}
+
+
 def combine_partials(vec, group=None):
     """All-reduce one rank's (L+2,) result tensor in place and return (totals, first_fail).
 
@@ -39,7 +42,16 @@ def combine_partials(vec, group=None):
         dist.all_reduce(vec[:L + 1], op=dist.ReduceOp.SUM, group=group)
     # ONE device-to-host copy (and one synchronisation) per evaluation; the branch on the summed failure
     # count is taken on the host, identically on every rank
-    host = vec.detach().to("cpu", torch.float64).numpy().copy()
+    if vec.is_cuda:  # pinned staging buffer + one stream synchronisation (a pageable .to("cpu") costs ~20 us more)
+        key = (vec.device.index, vec.shape[0])
+        stage = _PINNED.get(key)
+        if stage is None:
+            stage = _PINNED[key] = torch.empty(vec.shape[0], dtype=torch.float64).pin_memory()
+        stage.copy_(vec.detach(), non_blocking=True)
+        torch.cuda.current_stream(vec.device).synchronize()
+        host = stage.numpy().copy()
+    else:
+        host = vec.detach().to(torch.float64).numpy().copy()
     if multi and host[L] > 0.0:  # rare: somebody failed -- recover the lowest failing index
         dist.all_reduce(vec[L + 1:], op=dist.ReduceOp.MAX, group=group)
         host[L + 1] = float(vec[L + 1])

@@ -102,6 +102,23 @@ def _torch():
     return torch
 
 
+_STREAMS: dict = {}
+
+
+def _device_streams(torch, device):
+    """One (compute, upload) stream pair per device, created once.  A fresh pair per problem made the first ~16
+    problems of a process slow (torch hands out 32 pool streams round-robin and the first use of each costs
+    10-30 ms with this library loaded: measured in bench.py's end-to-end leg); problems on one device share the
+    pair, i.e. their device work serialises, which is what a single GPU does with it anyway."""
+    key = (device.type, device.index)
+    pair = _STREAMS.get(key)
+    if pair is None:
+        with torch.cuda.device(device):
+            pair = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
+        _STREAMS[key] = pair
+    return pair
+
+
 class DeviceProblem:
     """Device-resident inputs of one dataset (or one contiguous shard of its rows).
 
@@ -140,7 +157,7 @@ class DeviceProblem:
             # A private (non-blocking) stream: the legacy default stream would serialise the library's
             # work against the side-stream upload of the neighbor table.  Consumers on other streams are
             # ordered behind it with an event (see _publish).
-            self._stream = torch.cuda.Stream(device=self.device)
+            self._stream, side_stream = _device_streams(torch, self.device)
         with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
             stream = self._stream
             put = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=True)
@@ -151,7 +168,7 @@ class DeviceProblem:
             if rows > 0 and upload_chunks > 1:
                 host_nn = torch.from_numpy(np.ascontiguousarray(shard_rows))
                 self._nn = torch.empty((rows, self.mp1), dtype=torch.int64, device=self.device)
-                side = torch.cuda.Stream(device=self.device)
+                side = side_stream
                 side.wait_stream(self._stream)  # the block just handed out may still be in use by earlier work
                 self._nn.record_stream(side)
                 cuts = np.linspace(0, rows, upload_chunks + 1).astype(np.int64)
