@@ -131,7 +131,7 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab)
     const int ki = __double2loint(kf);
     const double kd = kf - 6755399441055744.0;
     double r = fma(kd, -0.021660849335603416, -x);   // ln2/32 split hi (low 24 bits clear) ...
-    r = fma(kd, -5.689487495325457e-11, r);          // ... + lo
+    r = fma(kd, -5.689487495325457e-11, r);          // ... + lo (a single-FMA reduction was measured: no faster)
     double q = fma(r, 1.0 / 720.0, 1.0 / 120.0);
     q = fma(q, r, 1.0 / 24.0);
     q = fma(q, r, 1.0 / 6.0);

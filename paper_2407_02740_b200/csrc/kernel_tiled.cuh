@@ -405,6 +405,9 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
     load_rec(nidx, nrec);
 #elif TILED_PREFETCH == 2
     load_idx((int64_t)blockIdx.x * TILED_WPB + warp, nidx);
+#elif TILED_PREFETCH == 3
+    load_idx((int64_t)blockIdx.x * TILED_WPB + warp, nidx);
+    load_rec(nidx, nrec);
 #endif
     // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
     for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         //      the diagonal holds zeros). ----
         phase_sync();
         PHASE_MARK(2);
-#if TILED_PREFETCH
+#if TILED_PREFETCH == 1 || TILED_PREFETCH == 2
         load_idx(batch + stride, nidx); // next batch of this warp (see the gather pipeline above)
 #endif
         double sb[S], eb[S], rr[QD + 1][S];
@@ -990,6 +993,10 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         PHASE_MARK(4);
 #if TILED_PREFETCH == 1
         load_rec(nidx, nrec);
+#elif TILED_PREFETCH == 3
+        // the whole gather of the NEXT batch inside the contraction of this one (the rows of K are dead here, so
+        // the 20 registers are free): indices now, records at the end of the loop body
+        load_idx(batch + stride, nidx);
 #elif TILED_PREFETCH == 2
 #pragma unroll
         for (int s = 0; s < S; ++s)
@@ -1084,6 +1091,9 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             if (E.fail_rows)
                 E.fail_rows[i - E.i0] = failpiv - pad;
         }
+#if TILED_PREFETCH == 3
+        load_rec(nidx, nrec);
+#endif
         phase_sync();
         PHASE_MARK(5);
     }

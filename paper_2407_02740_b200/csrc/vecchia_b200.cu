@@ -14,6 +14,7 @@
 #include "kernel_warp_smem.cuh"
 #include "kernel_thread.cuh"
 #include "tiled_host.cuh"
+#include "kernel_krige_generic.cuh"
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -925,6 +926,23 @@ extern "C" int vb200_last_kernel_ms(vb200_problem *P, double *ms)
     return VB200_OK;
 }
 
+// Launch configuration of the shape-agnostic kriging kernel: warps per block (<= 4) such that the block's shared
+// memory fits, blocks per SM from the occupancy query.  Returns 0, VB200_EUNSUPPORTED or -100 (CUDA error pending).
+static int krige_generic_config(const vb200_problem *P, int family, int m_pred, krige_generic_kernel_t *kern, int *warps,
+                                size_t *smem, int *per_sm)
+{
+    const size_t per_warp = sizeof(double) * (size_t)krige_generic_doubles(m_pred + 1, P->d);
+    int w = 4;
+    while (w > 1 && (size_t)w * per_warp > P->smem_optin)
+        w >>= 1;
+    if ((size_t)w * per_warp > P->smem_optin)
+        return VB200_EUNSUPPORTED;
+    *kern = krige_generic_for(family);
+    *warps = w;
+    *smem = (size_t)w * per_warp;
+    return kernel_blocks_per_sm((const void *)*kern, 32 * w, *smem, true, per_sm);
+}
+
 // stream-ordered temporaries that are released on EVERY exit path of a function (round 1 leaked them when a
 // CUDA call in the middle failed)
 struct AsyncFreeGuard {
@@ -960,11 +978,20 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
     if (npred == 0)
         return VB200_OK;
     const KrigeInstance *inst = krige_find(family, m_pred, P->d);
-    if (!inst)
-        return fail(VB200_EUNSUPPORTED, "no kriging kernel for this family / dimension / m_pred (d in {2,3}, m_pred <= 62)");
-    E.pair_tab = tiled_pair_table(inst->g, inst->s);
-    if (!E.pair_tab)
-        return fail(VB200_ECUDA, "pair table allocation failed");
+    krige_generic_kernel_t gkern = nullptr;
+    int gwarps = 0, gper_sm = 0;
+    size_t gsmem = 0;
+    if (!inst) { // any other shape: the generic warp-per-point kernel
+        const int rcg = krige_generic_config(P, family, m_pred, &gkern, &gwarps, &gsmem, &gper_sm);
+        if (rcg == VB200_EUNSUPPORTED)
+            return fail(VB200_EUNSUPPORTED, "m_pred too large for the shared memory of this device");
+        if (rcg)
+            return fail(VB200_ECUDA, std::string("kriging launch setup: ") + cudaGetErrorString(cudaGetLastError()));
+    } else {
+        E.pair_tab = tiled_pair_table(inst->g, inst->s);
+        if (!E.pair_tab)
+            return fail(VB200_ECUDA, "pair table allocation failed");
+    }
     KrigeParams K;
     memset(&K, 0, sizeof(K));
     K.npred = npred;
@@ -997,23 +1024,28 @@ extern "C" int vb200_krige(vb200_problem *P, int family, const double *theta, in
     K.mean_resid = d_out;
     K.var = d_out + npred;
     reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
-    const size_t smem = (size_t)inst->smem_doubles * sizeof(double);
-    if (smem > P->smem_optin)
-        return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
-    CUDA_TRY(cudaFuncSetAttribute(inst->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaFuncSetAttribute(inst->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inst->kernel, 32, smem));
-    if (per_sm < 1)
-        per_sm = 1;
-    const int opw = 32 / inst->g;
-    const int64_t nbatch = (npred + opw - 1) / opw;
-    int64_t blocks = (int64_t)P->sm_count * per_sm;
-    if (blocks > nbatch)
-        blocks = nbatch;
-    inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+    if (inst) {
+        const size_t smem = (size_t)inst->smem_doubles * sizeof(double);
+        if (smem > P->smem_optin)
+            return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
+        int per_sm = 0;
+        if (kernel_blocks_per_sm((const void *)inst->kernel, 32, smem, true, &per_sm))
+            return fail(VB200_ECUDA, std::string("kriging launch setup: ") + cudaGetErrorString(cudaGetLastError()));
+        const int opw = 32 / inst->g;
+        const int64_t nbatch = (npred + opw - 1) / opw;
+        int64_t blocks = (int64_t)P->sm_count * per_sm;
+        if (blocks > nbatch)
+            blocks = nbatch;
+        inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+        P->last_kernel = inst->name;
+    } else {
+        int64_t blocks = (int64_t)P->sm_count * gper_sm;
+        if (blocks > (npred + gwarps - 1) / gwarps)
+            blocks = (npred + gwarps - 1) / gwarps;
+        gkern<<<(unsigned)blocks, 32 * gwarps, gsmem, P->stream>>>(E, K);
+        P->last_kernel = "vecchia_krige_generic_kernel";
+    }
     CUDA_TRY(cudaGetLastError());
-    P->last_kernel = inst->name;
     P->last_launches = 2;
     if (int rc0 = ensure_host_fail(P))
         return rc0;
@@ -1052,11 +1084,20 @@ extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta,
     if (m_pred < 1)
         return fail(VB200_EINVAL, "simulation needs at least one neighbour column");
     const KrigeInstance *inst = krige_find(family, m_pred, P->d);
-    if (!inst)
-        return fail(VB200_EUNSUPPORTED, "no kriging kernel for this family / dimension / m (d in {2,3}, m <= 62)");
-    E.pair_tab = tiled_pair_table(inst->g, inst->s);
-    if (!E.pair_tab)
-        return fail(VB200_ECUDA, "pair table allocation failed");
+    krige_generic_kernel_t gkern = nullptr;
+    int gwarps = 0, gper_sm = 0;
+    size_t gsmem = 0;
+    if (!inst) {
+        const int rcg = krige_generic_config(P, family, m_pred, &gkern, &gwarps, &gsmem, &gper_sm);
+        if (rcg == VB200_EUNSUPPORTED)
+            return fail(VB200_EUNSUPPORTED, "m too large for the shared memory of this device");
+        if (rcg)
+            return fail(VB200_ECUDA, std::string("simulation launch setup: ") + cudaGetErrorString(cudaGetLastError()));
+    } else {
+        E.pair_tab = tiled_pair_table(inst->g, inst->s);
+        if (!E.pair_tab)
+            return fail(VB200_ECUDA, "pair table allocation failed");
+    }
     KrigeParams K;
     memset(&K, 0, sizeof(K));
     K.m_pred = m_pred;
@@ -1079,16 +1120,16 @@ extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta,
     K.sim_y = d_y;
     K.rec_w = P->rec;
     reset_fail_kernel<<<1, 1, 0, P->stream>>>(P->fail_word, P->fail_count);
-    const size_t smem = (size_t)inst->smem_doubles * sizeof(double);
-    if (smem > P->smem_optin)
-        return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
-    CUDA_TRY(cudaFuncSetAttribute(inst->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaFuncSetAttribute(inst->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inst->kernel, 32, smem));
-    if (per_sm < 1)
-        per_sm = 1;
-    const int opw = 32 / inst->g;
+    size_t smem = gsmem;
+    int per_sm = gper_sm;
+    if (inst) {
+        smem = (size_t)inst->smem_doubles * sizeof(double);
+        if (smem > P->smem_optin)
+            return fail(VB200_EUNSUPPORTED, "kriging tier exceeds shared memory");
+        if (kernel_blocks_per_sm((const void *)inst->kernel, 32, smem, true, &per_sm))
+            return fail(VB200_ECUDA, std::string("simulation launch setup: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    const int opw = inst ? 32 / inst->g : gwarps;
     // one launch per dependency level: the observations of a level only read values of lower levels,
     // written by earlier launches on the same stream
     for (int64_t l = 0; l < nlevels; ++l) {
@@ -1101,10 +1142,13 @@ extern "C" int vb200_simulate(vb200_problem *P, int family, const double *theta,
         int64_t blocks = (int64_t)P->sm_count * per_sm;
         if (blocks > nbatch)
             blocks = nbatch;
-        inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+        if (inst)
+            inst->kernel<<<(unsigned)blocks, 32, smem, P->stream>>>(E, K);
+        else
+            gkern<<<(unsigned)blocks, 32 * gwarps, smem, P->stream>>>(E, K);
     }
     CUDA_TRY(cudaGetLastError());
-    P->last_kernel = inst->name;
+    P->last_kernel = inst ? inst->name : "vecchia_krige_generic_kernel";
     P->last_launches = 1 + (int)nlevels;
     if (int rc0 = ensure_host_fail(P))
         return rc0;

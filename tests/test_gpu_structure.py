@@ -370,3 +370,48 @@ def test_engine_run_sees_in_place_edits_of_the_dataset():
     b = engine.run(ds, nn, cov)
     assert b.ysy == pytest.approx(4.0 * a.ysy, rel=1e-12)
     assert b.logdet == a.logdet
+
+
+# ---------------------------------------------------------------------------
+# shapes outside the tiled kriging instances (d = 1, d = 4, m_pred > 62): the generic warp-per-point kernel
+# (the reference's predict.krige / simulate_nn_gp accept any d and any m_pred <= n)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("family,d,theta,m_pred", [("exponential_isotropic", 1, [1.2, 0.1, 0.1], 12),
+                                                   ("matern15_isotropic", 4, [1.0, 0.4, 0.05], 25),
+                                                   ("exponential_anisotropic", 4, [1.3, 0.3, 0.4, 0.5, 0.6, 0.1], 20),
+                                                   ("matern25_isotropic", 2, [0.8, 0.15, 0.02], 90),
+                                                   ("matern_isotropic", 1, [1.0, 0.2, 0.8, 0.05], 10)])
+def test_kriging_generic_shapes_against_oracle(family, d, theta, m_pred):
+    from oracle import vecchia_oracle as vo
+    rng = np.random.default_rng(18)
+    n, npred = 1500, 200
+    y, X, locs, theta = make_instance(654, n, d, 2, family, theta)
+    star = rng.uniform(0, 1, (npred, d))
+    Xs = np.column_stack([np.ones(npred), rng.normal(size=npred)])
+    beta = np.array([0.3, -0.7])
+    cov = vg.CovarianceParameters(family, theta)
+    fr = vg.FitResult(theta_hat=cov, beta_hat=beta, beta_cov=np.eye(2), loglik_trace=[0.0],
+                      fisher_info=np.eye(cov.nparms), iterations=0, converged=True)
+    for latent in (False, True):
+        ps = vg.krige(fr, vg.Dataset(y, X, locs), star, Xs, m_pred=m_pred, latent=latent)
+        mean, sd, _ = vo.krige(y, X, locs, family, theta, beta, star, Xs, m_pred, latent=latent)
+        np.testing.assert_allclose(ps.mean, mean, rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(ps.sd ** 2, sd ** 2, rtol=1e-9, atol=1e-11)
+
+
+@pytest.mark.parametrize("family,d,theta,m", [("exponential_isotropic", 1, [1.2, 0.1, 0.1], 8),
+                                              ("matern15_isotropic", 4, [1.0, 0.4, 0.05], 15),
+                                              ("exponential_isotropic", 2, [1.5, 0.2, 0.1], 70)])
+def test_simulation_generic_shapes_against_oracle(family, d, theta, m):
+    from oracle import numpy_families as nf
+    rng = np.random.default_rng(6)
+    n = 500
+    locs = rng.uniform(0, 1, (n, d))
+    X = np.column_stack([np.ones(n), rng.normal(size=n)])
+    beta = np.array([0.4, -1.1])
+    nn = vg.find_ordered_neighbors(locs, m)
+    cov = vg.CovarianceParameters(family, theta)
+    y = vg.simulate_nn_gp(cov, beta, locs, X, nn, seed=31)
+    want = nf.simulate_nn_gp(family, np.asarray(theta, dtype=np.float64), beta,
+                             vg.covariance_registry(family).prepare_locs(locs), X, nn.idx, 31)
+    np.testing.assert_allclose(y, want, rtol=1e-9, atol=1e-9)
