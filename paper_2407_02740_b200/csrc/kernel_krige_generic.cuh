@@ -1,7 +1,7 @@
 // kernel_krige_generic.cuh -- shape-agnostic nearest-neighbour kriging / conditional simulation.
 //
 // The tiled kriging kernel (kernel_krige.cuh) is instantiated for d in {2, 3} and m_pred <= 62; the reference's
-// predict.krige (/root/reference/pkg/src/vecchiagp/predict.py:35-90) and simulate_nn_gp (oracle.py:102-140) accept
+// predict.krige (/root/reference/pkg/src/vecchiagp/predict.py:35-90) and simulate_nn_gp (file:line in include/vecchia_b200.h) accept
 // any d and any m_pred <= n.  This kernel serves every other shape: ONE WARP per prediction point, the packed lower
 // triangle of the local matrix, the points and the right-hand side in shared memory, run-time d and m_pred (up to
 // the shared-memory capacity: m_pred + 1 <= ~230 on B200), lane-per-row square-root-free elimination.  Same local
