@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         // 115 cycles per step measured, profiles/r2_experiments.md).  NO masks: a lane whose row a is not
         // above l (a >= l) reads a finite, unrelated element of the store (colbase(a) + l stays inside it)
         // and pollutes sb only at and after its own step l = a, when sb has already been consumed; every lane
-        // receives every ut_l, writes it to shared memory (same value, same address within a group) and
+        // receives every ut_l, lane 0 of the group writes it to shared memory and every lane
         // reads its own entries back afterwards.
         double *us = pts; // CAP doubles: ut (the coordinate table is dead by now)
         {
@@ -870,7 +870,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                     constexpr int it = decltype(ic)::value, l = CAP - 1 - it;
                     constexpr int sl = l / G, ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
                     const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
-                    us[l] = ul;
+                    if (lg == 0) // every lane of the group holds the same ul; one of them stores it
+                        us[l] = ul;
 #pragma unroll
                     for (int s = 0; s < S; ++s)
                         if (s * G < l)

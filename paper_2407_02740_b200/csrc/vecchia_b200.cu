@@ -812,11 +812,15 @@ extern "C" int vb200_eval(vb200_problem *P, int family, const double *theta, int
     if (rc)
         return rc;
     CUDA_TRY(cudaMemcpyAsync(P->h_out, P->d_out, sizeof(double) * (L + 2), cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                             P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
     memcpy(out_sums, P->h_out, sizeof(double) * L);
-    const unsigned long long w = *P->h_fail;
+    unsigned long long w = ~0ull;
+    if (P->h_out[L] > 0.0) { // rare: fetch the latched failure word (index and pivot) as well
+        CUDA_TRY(cudaMemcpyAsync(P->h_fail, P->fail_word + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 P->stream));
+        CUDA_TRY(cudaStreamSynchronize(P->stream));
+        w = *P->h_fail;
+    }
     if (P->h_out[L] > 0.0 && w != ~0ull) {
         if (first_fail) *first_fail = (int64_t)(w >> 16);
         if (pivot) *pivot = (int32_t)(w & 0xffff) - 1;
