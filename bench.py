@@ -425,7 +425,7 @@ def ours_arm(args):
                 "ms_per_step": e2e_mean_ms, "ms_per_step_median": e2e_median_ms, "steps": e2e_steps,
                 "ms_each": [round(x, 2) for x in e2e_each], "ms_min": round(float(min(e2e_each)), 3),
                 "statistic": "mean over the timed steps (max of CUDA-event and host wall time)",
-                "path": "engine.DeviceProblem(pinned host y/X/locs/nn): table uploaded in 8 chunks on a side stream, vb200_create + vb200_eval_async per chunk behind the copies -> totals on the host"},
+                "path": "engine.DeviceProblem(pinned host y/X/locs/nn): table uploaded in 16 chunks on a side stream, vb200_create + vb200_eval_async per chunk behind the copies -> totals on the host"},
         "gpu_launches": launches, "roofline": roofline,
         "loglik": ev.loglik, "neighbor_search_s": t_nn, "rank_kernel_ms": rank_kernel_ms,
         "step_minus_kernel_us": 1000.0 * (ms_per_step - max(rank_kernel_ms)),
