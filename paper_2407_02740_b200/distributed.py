@@ -86,8 +86,15 @@ class ShardedEvaluator:
         vec = self.problem.totals_async(theta, self.jitter)
         totals, first = combine_partials(vec, self.group)
         if first >= 0:
-            lf, piv = self.problem.fail_info()
-            raise NotPositiveDefinite(pivot=piv if lf == first else -1, observation=first)
+            # the pivot is known on the rank that owns the failing row; an evaluation issued chunk by chunk behind
+            # the upload latches only its last piece's failure word, so ask the plain (single-launch) path
+            piv = -1
+            if self.i0 <= first < self.i1:
+                try:
+                    self.problem.totals(theta, self.jitter)
+                except NotPositiveDefinite as err:
+                    piv = err.pivot if err.observation == first else -1
+            raise NotPositiveDefinite(pivot=piv, observation=first)
         return totals
 
     def __call__(self, theta):
