@@ -25,6 +25,7 @@ struct MaternOrder {
     double nu, mu;
     double gam1, gam2;   // Temme's Gamma_1(mu), Gamma_2(mu)
     double gampl, gammi; // 1/Gamma(1+mu), 1/Gamma(1-mu)
+    double gp, gm;       // Gamma(1+mu), Gamma(1-mu) (the series starts from E Gamma(1+mu) / 2 and Gamma(1-mu) / (2 E))
     double fact;         // pi mu / sin(pi mu)
     double normcon;      // 2^(1-nu) / Gamma(nu)
     int nup, pad_;
@@ -154,25 +155,29 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab)
 #else
 #define VB_BESSEL_ATTR __forceinline__
 #endif
-static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double inv_x, const MaternOrder &M, double &knu,
-                                                  double &knum1)
+// `E` = exp(mu d) is supplied by the caller (the three orders of a pair differ by 1e-5, so two of the three
+// exponentials are a short Taylor factor); `nterms` <= VB_MATERN_TERMS is the warp-uniform series length for this x.
+static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double inv_x, const MaternOrder &M, const double E,
+                                                  const int nterms, double &knu, double &knum1)
 {
     const double mu = M.mu;
     double kmu, kmu1;
     if (x <= 2.0) {
         const double xh = 0.5 * x;
         const double e = mu * d;
-        const double E = exp(e), Ei = rcp_pos(E);
+        const double Ei = rcp_pos(E);
         const double e2 = e * e;
         // sinh(e)/e: series for small e, (E - 1/E) / (2e) otherwise
         const double shoe = (fabs(e) < 1e-2) ? fma(e2, fma(e2, 1.0 / 120.0, 1.0 / 6.0), 1.0)
                                              : 0.5 * (E - Ei) * M.inv_mu * rcp_pos(d);
         double ff = M.fact * fma(M.gam1, 0.5 * (E + Ei), M.gam2 * shoe * d);
         double sum = ff;
-        double p = 0.5 * E * rcp_pos(M.gampl), q = 0.5 * Ei * rcp_pos(M.gammi), c = 1.0, sum1 = p;
+        double p = 0.5 * E * M.gp, q = 0.5 * Ei * M.gm, c = 1.0, sum1 = p;
         const double d2 = xh * xh;
 #pragma unroll
-        for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
+        for (int i = 1; i <= VB_MATERN_TERMS; ++i) { // unrolled (static constant-bank indices), left early (uniform)
+            if (i > nterms)
+                break;
             ff = fma((double)i, ff, p + q) * M.r1[i - 1];
             c *= d2 * (1.0 / i);
             p *= M.rp[i - 1];
@@ -222,6 +227,16 @@ static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double i
     }
 }
 
+// Series length for this x (terms ~ (x/2)^(2i) / (i!)^2 against 1e-17), uniform over the lanes that are active
+// here (the callers' pair loops end raggedly, so the vote runs on the active mask).
+__device__ __forceinline__ int matern_series_terms(const double x)
+{
+    const unsigned am = __activemask();
+    const bool valid = x <= 2.0;
+    return __any_sync(am, valid && x > 1.0) ? VB_MATERN_TERMS
+           : (__any_sync(am, valid && x > 0.4) ? 10 : (__any_sync(am, valid && x > 0.1) ? 7 : 5));
+}
+
 // General Matern pair terms at scaled distance x = r/range: correlation 2^(1-nu)/Gamma(nu) x^nu K_nu(x),
 // its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative by a
 // central difference of step VB_MATERN_H (part of the family definition here; GpGp differentiates the
@@ -229,6 +244,7 @@ static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double i
 __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, double inv_rho, double &Kv, double &Drange,
                                              double &Dnu)
 {
+    const int nterms = matern_series_terms(x); // before any lane leaves
     if (x < 1e-60) { // coincident points: the x -> 0 limits
         Kv = P.sig2;
         Drange = 0.0;
@@ -243,15 +259,24 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
     }
     const double lx = log(x);
     const double d = 0.6931471805599453 - lx, inv_x = rcp_pos(x); // -log(x/2), 1/x: shared by the three orders
+    // exp(mu_t d) and x^nu_t for the three orders: the shifted orders differ from the central one by +-1e-5 in nu (and in
+    // mu, unless the shift crosses a half-integer), so exp(delta d) is a degree-5 Taylor factor (|delta d| < 2e-3)
+    auto small_exp = [](double z) {
+        return fma(z, fma(z, fma(z, fma(z, fma(z, 1.0 / 120.0, 1.0 / 24.0), 1.0 / 6.0), 0.5), 1.0), 1.0);
+    };
+    const double E0 = exp(P.mat[0].mu * d);
+    const double dm1 = P.mat[1].mu - P.mat[0].mu, dm2 = P.mat[2].mu - P.mat[0].mu; // uniform
+    const double E1 = (fabs(dm1) < 1e-3) ? E0 * small_exp(dm1 * d) : exp(P.mat[1].mu * d);
+    const double E2 = (fabs(dm2) < 1e-3) ? E0 * small_exp(dm2 * d) : exp(P.mat[2].mu * d);
     double k, km1, kp, km, unused;
-    bessel_k_pair(x, d, inv_x, P.mat[0], k, km1);
-    bessel_k_pair(x, d, inv_x, P.mat[1], kp, unused);
-    bessel_k_pair(x, d, inv_x, P.mat[2], km, unused);
+    bessel_k_pair(x, d, inv_x, P.mat[0], E0, nterms, k, km1);
+    bessel_k_pair(x, d, inv_x, P.mat[1], E1, nterms, kp, unused);
+    bessel_k_pair(x, d, inv_x, P.mat[2], E2, nterms, km, unused);
     const double xn = exp(P.mat[0].nu * lx);
     Kv = P.sig2 * P.mat[0].normcon * xn * k;
     Drange = P.sig2 * P.mat[0].normcon * xn * x * km1 * inv_rho;
-    const double cp = P.mat[1].normcon * exp(P.mat[1].nu * lx) * kp;
-    const double cm = P.mat[2].normcon * exp(P.mat[2].nu * lx) * km;
+    const double cp = P.mat[1].normcon * (xn * small_exp((P.mat[1].nu - P.mat[0].nu) * lx)) * kp;
+    const double cm = P.mat[2].normcon * (xn * small_exp((P.mat[2].nu - P.mat[0].nu) * lx)) * km;
     Dnu = P.sig2 * (cp - cm) * (0.5 / VB_MATERN_H);
 }
 

@@ -92,7 +92,9 @@ __device__ __forceinline__ void pair_terms_r(const EvalParams &E, const double *
 #pragma unroll
         for (int l = 0; l < D; ++l)
             x2 = fma(dl[l], dl[l], x2);
-        matern_terms_call(E, x2 * rsqrt_pos(x2), Kv, Dv[0], Dv[1]);
+        // inlined: the general Matern only runs the ROLLED pair-table pair phase, and an out-of-line callee would take
+        // the kernel parameters by address, i.e. from a local-memory copy instead of the constant bank (measured 2x)
+        matern_terms(E, x2 * rsqrt_pos(x2), E.inv_rho[0], Kv, Dv[0], Dv[1]);
     } else if constexpr (FAM == FAM_EXP_ISO || FAM == FAM_MATERN15 || FAM == FAM_MATERN25) {
         double x2 = 1e-300;
 #pragma unroll
@@ -497,7 +499,9 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             // ---- pair-table pair phase.  The table lists the off-diagonal pairs (a > c) by DESCENDING c, so the
             //      k(k-1)/2 pairs among the live points come first; the rest is zero-filled. ----
             using TS = TileSmem<G, S, D, QD>;
-            constexpr int NI = TS::NI;
+            // pairs in flight per lane: two for the closed forms; ONE for the general Matern, whose Bessel evaluations
+            // are long enough to spill when two are interleaved (measured 38 ms against 50 ms per evaluation)
+            constexpr int NI = (FAM == FAM_MATERN) ? 1 : TS::NI;
             const int nlp = nlive * (nlive - 1) / 2;
             unsigned nxt[NI];
 #pragma unroll

@@ -35,9 +35,11 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
             const double x = x2 * rsqrt_pos(x2);
             double k, km1;
             Kv = E.sig2;
+            const int nterms = matern_series_terms(x);
             if (x >= 1e-60) {
                 const double lx = log(x);
-                bessel_k_pair(x, 0.6931471805599453 - lx, rcp_pos(x), E.mat[0], k, km1);
+                const double dd = 0.6931471805599453 - lx;
+                bessel_k_pair(x, dd, rcp_pos(x), E.mat[0], exp(E.mat[0].mu * dd), nterms, k, km1);
                 Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * lx) * k;
             }
             Dv[0] = Dv[1] = 0.0;

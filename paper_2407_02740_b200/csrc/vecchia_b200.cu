@@ -432,6 +432,8 @@ static MaternOrder matern_order(double nu)
     const long double gp = 1.0L / tgammal(1.0L + mu), gm = 1.0L / tgammal(1.0L - mu);
     M.gampl = (double)gp;
     M.gammi = (double)gm;
+    M.gp = (double)tgammal(1.0L + mu);
+    M.gm = (double)tgammal(1.0L - mu);
     M.gam2 = (double)(0.5L * (gm + gp));
     if (fabsl(mu) < 1e-4L)
         M.gam1 = (double)(-(0.5772156649015328606L - 0.0420026350340952L * mu * mu));
