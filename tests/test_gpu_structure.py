@@ -415,3 +415,32 @@ def test_simulation_generic_shapes_against_oracle(family, d, theta, m):
     want = nf.simulate_nn_gp(family, np.asarray(theta, dtype=np.float64), beta,
                              vg.covariance_registry(family).prepare_locs(locs), X, nn.idx, 31)
     np.testing.assert_allclose(y, want, rtol=1e-9, atol=1e-9)
+
+
+# ---------------------------------------------------------------------------
+# housekeeping entry points of the C ABI added in round 2
+# ---------------------------------------------------------------------------
+def test_one_launch_per_evaluation_fallback_counter_and_memory_release():
+    lib = _cabi.load()
+    y, X, locs, _ = make_instance(77, 2000, 2, 1)
+    nn = vg.find_ordered_neighbors(locs, 30)
+    theta = np.array([1.5, 0.25, 0.1])
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "exponential_isotropic") as prob:
+        a = prob.totals(theta)
+        assert prob.last_launch_count == 1, "reset, main kernel and reduction are ONE launch"
+        assert prob.layout_for(3) == "tiled_reg"
+        before = lib.vb200_fallback_count()
+        prob.totals(theta)
+        assert lib.vb200_fallback_count() == before, "a tiled instance exists: no fallback"
+        assert np.array_equal(a, prob.totals(theta))
+    # a shape without a tiled instance (p = 5): AUTO falls back, says so once, and counts it
+    y5, X5, locs5, _ = make_instance(78, 800, 2, 5)
+    nn5 = vg.find_ordered_neighbors(locs5, 12)
+    engine._FALLBACK_WARNED.clear()
+    with DeviceProblem(vg.Dataset(y5, X5, locs5), nn5, "exponential_isotropic") as prob:
+        before = lib.vb200_fallback_count()
+        with pytest.warns(RuntimeWarning, match="falling back"):
+            prob.totals(theta)
+        assert prob.layout_for(3) == "warp_smem"
+        assert lib.vb200_fallback_count() == before + 1
+    assert lib.vb200_release_memory(0) == 0
