@@ -73,10 +73,18 @@ def _scaled_distance(a, b, rho):
     return np.sqrt(np.einsum("ijk,ijk->ij", diff, diff)), diff
 
 
-def _matern_corr(nu, x):
-    from scipy.special import gammaln, kv
+def _log_xk(order, power, x):
+    """log( x^power K_order(x) ) in log space (exponentially scaled Bessel function): K_nu(x) overflows for large nu at
+    small x while x^nu underflows, their product is O(1)."""
+    from scipy.special import kve
     with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
-        out = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + nu * np.log(x)) * kv(nu, x)
+        return power * np.log(x) + np.log(kve(order, x)) - x
+
+
+def _matern_corr(nu, x):
+    from scipy.special import gammaln
+    with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+        out = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + _log_xk(nu, nu, x))
     return np.where(x < 1e-60, 1.0, out)
 
 
@@ -149,9 +157,9 @@ class CovarianceFamily:
                 D[1] = sum(per_axis[:-1])
                 D[2] = per_axis[-1]
         elif self.kernel_code == KERNEL_MATERN:
-            from scipy.special import gammaln, kv
+            from scipy.special import gammaln
             with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
-                drho = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + (nu + 1.0) * np.log(s)) * kv(nu - 1.0, s) / rho[0]
+                drho = np.exp((1.0 - nu) * np.log(2.0) - gammaln(nu) + _log_xk(abs(nu - 1.0), nu + 1.0, s)) / rho[0]
             D[1] = sig2 * np.where(s < 1e-60, 0.0, drho)
             D[2] = sig2 * (_matern_corr(nu + MATERN_H, s) - _matern_corr(nu - MATERN_H, s)) / (2.0 * MATERN_H)
         elif self.kernel_code == KERNEL_MATERN15:

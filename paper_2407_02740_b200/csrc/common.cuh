@@ -28,6 +28,7 @@ struct MaternOrder {
     double gp, gm;       // Gamma(1+mu), Gamma(1-mu) (the series starts from E Gamma(1+mu) / 2 and Gamma(1-mu) / (2 E))
     double fact;         // pi mu / sin(pi mu)
     double normcon;      // 2^(1-nu) / Gamma(nu)
+    double nc2;          // 2 / Gamma(nu): correlation = nc2 (x/2)^nu K_nu(x)
     int nup, pad_;
     double inv_mu;       // 1/mu (0 when mu == 0; only used for |mu d| >= 1e-2)
     // reciprocals that depend on (iteration, mu) only -- the divisions of Temme's series and of
@@ -157,15 +158,20 @@ __device__ __forceinline__ double exp_neg(double x, const double *tab)
 #endif
 // `E` = exp(mu d) is supplied by the caller (the three orders of a pair differ by 1e-5, so two of the three
 // exponentials are a short Taylor factor); `nterms` <= VB_MATERN_TERMS is the warp-uniform series length for this x.
+// Outputs are SCALED so that nothing overflows for large orders at small x (K_nu(x) ~ Gamma(nu)/2 (2/x)^nu does):
+//   tnu = (x/2)^nu K_nu(x)          (-> Gamma(nu)/2 as x -> 0: bounded by ~1e80 for nu <= 60)
+//   bq  = (x/2)^(nu+1) K_(nu-1)(x)
+// with the upward recurrence run on T_a = (x/2)^a K_a:  T_(a+1) = a T_a + (x/2)^2 T_(a-1).  The Matern correlation is
+// then 2 tnu / Gamma(nu) and its range derivative 4 bq / Gamma(nu) / range -- no x^nu factor is ever formed.
 static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double inv_x, const MaternOrder &M, const double E,
-                                                  const int nterms, double &knu, double &knum1)
+                                                  const int nterms, double &tnu, double &bq)
 {
     const double mu = M.mu;
     double kmu, kmu1;
+    const double xh = 0.5 * x, d2 = xh * xh;
+    const double Ei = rcp_pos(E); // (x/2)^mu
     if (x <= 2.0) {
-        const double xh = 0.5 * x;
         const double e = mu * d;
-        const double Ei = rcp_pos(E);
         const double e2 = e * e;
         // sinh(e)/e: series for small e, (E - 1/E) / (2e) otherwise
         const double shoe = (fabs(e) < 1e-2) ? fma(e2, fma(e2, 1.0 / 120.0, 1.0 / 6.0), 1.0)
@@ -173,7 +179,6 @@ static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double i
         double ff = M.fact * fma(M.gam1, 0.5 * (E + Ei), M.gam2 * shoe * d);
         double sum = ff;
         double p = 0.5 * E * M.gp, q = 0.5 * Ei * M.gm, c = 1.0, sum1 = p;
-        const double d2 = xh * xh;
 #pragma unroll
         for (int i = 1; i <= VB_MATERN_TERMS; ++i) { // unrolled (static constant-bank indices), left early (uniform)
             if (i > nterms)
@@ -212,18 +217,19 @@ static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double i
         kmu = sqrt(1.5707963267948966 * inv_x) * exp(-x) / s;
         kmu1 = kmu * (mu + x + 0.5 - a1 * h) * inv_x;
     }
+    const double s1 = Ei * xh; // (x/2)^(mu+1)
     if (M.nup == 0) {
-        knu = kmu;
-        knum1 = fma(-2.0 * mu * inv_x, kmu, kmu1); // K_{mu-1}
+        tnu = Ei * kmu;
+        bq = s1 * fma(-2.0 * mu * inv_x, kmu, kmu1); // (x/2)^(mu+1) K_(mu-1)
     } else {
-        double prev = kmu, cur = kmu1;
+        double prev = Ei * kmu, cur = s1 * kmu1;     // T_mu, T_(mu+1)
         for (int i = 1; i < M.nup; ++i) {
-            const double next = fma(2.0 * (mu + i) * inv_x, cur, prev);
+            const double next = fma(mu + i, cur, d2 * prev);
             prev = cur;
             cur = next;
         }
-        knu = cur;
-        knum1 = prev;
+        tnu = cur;
+        bq = d2 * prev;
     }
 }
 
@@ -268,16 +274,14 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
     const double dm1 = P.mat[1].mu - P.mat[0].mu, dm2 = P.mat[2].mu - P.mat[0].mu; // uniform
     const double E1 = (fabs(dm1) < 1e-3) ? E0 * small_exp(dm1 * d) : exp(P.mat[1].mu * d);
     const double E2 = (fabs(dm2) < 1e-3) ? E0 * small_exp(dm2 * d) : exp(P.mat[2].mu * d);
-    double k, km1, kp, km, unused;
-    bessel_k_pair(x, d, inv_x, P.mat[0], E0, nterms, k, km1);
-    bessel_k_pair(x, d, inv_x, P.mat[1], E1, nterms, kp, unused);
-    bessel_k_pair(x, d, inv_x, P.mat[2], E2, nterms, km, unused);
-    const double xn = exp(P.mat[0].nu * lx);
-    Kv = P.sig2 * P.mat[0].normcon * xn * k;
-    Drange = P.sig2 * P.mat[0].normcon * xn * x * km1 * inv_rho;
-    const double cp = P.mat[1].normcon * (xn * small_exp((P.mat[1].nu - P.mat[0].nu) * lx)) * kp;
-    const double cm = P.mat[2].normcon * (xn * small_exp((P.mat[2].nu - P.mat[0].nu) * lx)) * km;
-    Dnu = P.sig2 * (cp - cm) * (0.5 / VB_MATERN_H);
+    double t0, b0, tp, tm, unused;
+    bessel_k_pair(x, d, inv_x, P.mat[0], E0, nterms, t0, b0);
+    bessel_k_pair(x, d, inv_x, P.mat[1], E1, nterms, tp, unused);
+    bessel_k_pair(x, d, inv_x, P.mat[2], E2, nterms, tm, unused);
+    // correlation 2^(1-nu)/Gamma(nu) x^nu K_nu = nc2 (x/2)^nu K_nu with nc2 = 2/Gamma(nu)
+    Kv = P.sig2 * P.mat[0].nc2 * t0;
+    Drange = P.sig2 * (2.0 * P.mat[0].nc2) * b0 * inv_rho; // sigma^2 nc x^(nu+1) K_(nu-1) / range
+    Dnu = P.sig2 * fma(P.mat[1].nc2, tp, -(P.mat[2].nc2 * tm)) * (0.5 / VB_MATERN_H);
 }
 
 // Out-of-line entry for the fully unrolled row-owner pair phase of kernel_tiled.cuh (keeps ~60 copies of

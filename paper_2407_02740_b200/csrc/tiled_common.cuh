@@ -40,7 +40,7 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
                 const double lx = log(x);
                 const double dd = 0.6931471805599453 - lx;
                 bessel_k_pair(x, dd, rcp_pos(x), E.mat[0], exp(E.mat[0].mu * dd), nterms, k, km1);
-                Kv = E.sig2 * E.mat[0].normcon * exp(E.mat[0].nu * lx) * k;
+                Kv = E.sig2 * E.mat[0].nc2 * k; // k = (x/2)^nu K_nu(x)
             }
             Dv[0] = Dv[1] = 0.0;
         }

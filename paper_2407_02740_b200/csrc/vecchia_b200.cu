@@ -442,6 +442,7 @@ static MaternOrder matern_order(double nu)
     const long double pimu = 3.14159265358979323846264338L * mu;
     M.fact = (fabsl(pimu) < 1e-9L) ? 1.0 : (double)(pimu / sinl(pimu));
     M.normcon = std::exp((1.0 - nu) * 0.6931471805599453 - std::lgamma(nu));
+    M.nc2 = std::exp(0.6931471805599453 - std::lgamma(nu));
     M.inv_mu = M.mu != 0.0 ? 1.0 / M.mu : 0.0;
     for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
         M.r1[i - 1] = (double)(1.0L / ((long double)i * i - mu * mu));

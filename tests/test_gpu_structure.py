@@ -444,3 +444,36 @@ def test_one_launch_per_evaluation_fallback_counter_and_memory_release():
         assert prob.layout_for(3) == "warp_smem"
         assert lib.vb200_fallback_count() == before + 1
     assert lib.vb200_release_memory(0) == 0
+
+
+def test_general_matern_large_smoothness_small_distances_stay_finite():
+    """nu = 45 at scaled distances down to ~1e-4: K_nu(x) itself is ~1e250 there, x^nu ~1e-180; the device works with
+    (x/2)^nu K_nu (bounded) and must agree with a log-space evaluation of the same correlation (advisor finding,
+    round 1: the unscaled recurrence overflowed to inf * 0 = NaN)."""
+    from scipy.special import gammaln, kve
+    rng = np.random.default_rng(12)
+    n, m = 400, 12
+    locs = rng.uniform(0, 1, (n, 2)) * 1e-3          # tiny domain ...
+    locs[::7] += rng.uniform(0, 1, (locs[::7].shape[0], 2)) * 1e-6
+    theta = np.array([1.0, 1.0, 45.0, 0.05])          # ... against range 1: x in [1e-6, 1.4e-3]
+    y, X = rng.normal(size=n), np.ones((n, 1))
+    nn = vg.find_ordered_neighbors(locs, m)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern_isotropic") as prob:
+        for layout in _layouts(prob, 4):
+            prob.set_layout(layout)
+            tot = prob.totals(theta)
+            assert np.all(np.isfinite(tot)), layout
+    # one observation against a log-space dense evaluation: conditional variance of point 30 given its neighbours
+    i = 30
+    idx = nn.idx[i][nn.idx[i] >= 0][::-1]              # local frame: neighbours ..., observation last
+    P = locs[idx]
+    r = np.sqrt(((P[:, None, :] - P[None, :, :]) ** 2).sum(-1)) / theta[1]
+    nu = theta[2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        logc = (1.0 - nu) * np.log(2.0) - gammaln(nu) + nu * np.log(r) + np.log(kve(nu, r)) - r
+    K = theta[0] * np.where(r > 0, np.exp(logc), 1.0) + theta[0] * theta[3] * np.eye(len(idx))
+    want = np.log(1.0 / np.linalg.inv(K)[-1, -1])
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern_isotropic") as prob:
+        rows, flags = prob.rows_host(theta, 0.0, i, i + 1)
+    assert flags[0] == 0
+    assert rows[0][0] == pytest.approx(want, rel=1e-6, abs=1e-6)   # logdet contribution = log of the conditional variance
