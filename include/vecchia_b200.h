@@ -188,7 +188,8 @@ int vb200_last_launch_count(const vb200_problem *prob);
 const char *vb200_last_kernel_name(const vb200_problem *prob);
 
 /* Enumerate the compiled TILED_REG kernel instances (for tests and tooling): instance k serves
- * `family` with exactly d coordinates and p design columns, for any m+1 <= cap-1. */
+ * `family` with exactly d coordinates and p design columns, for any m+1 <= cap-1 (cap = rows of the packed
+ * local triangle: lanes_per_obs * rows_per_lane minus the instance's static padding rows beyond the first). */
 int vb200_tiled_instance_count(void);
 int vb200_tiled_instance(int k, int *lanes_per_obs, int *rows_per_lane, int *cap, int *family, int *d, int *p);
 

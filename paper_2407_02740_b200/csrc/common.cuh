@@ -119,29 +119,51 @@ __device__ __forceinline__ double sqrt_pos(double a)
     return fma(d, 0.5 * y, g);
 }
 
-#define VB_EXPTAB 32 // entries of 2^(j/32) in shared memory
+#ifndef VB_EXPTAB
+#define VB_EXPTAB 32 // entries of 2^(j/VB_EXPTAB) in shared memory (32 or 64)
+#endif
 
-// exp(-x) for x >= 0: -x = k ln2/32 + r, |r| <= ln2/64; 2^(k/32) from a 32-entry table and the
-// exponent field, e^r from a degree-6 polynomial (truncation 3.4e-18).  Max relative error
-// ~2e-16 against libm; x is clamped at ~700 (result ~1e-304, never denormal).
+// exp(-x) for x >= 0: -x = k ln2/N + r, |r| <= ln2/2N (N = VB_EXPTAB); 2^(k/N) from an N-entry table and the
+// exponent field, e^r from a polynomial.  N = 32, degree 5: truncation r^6/720 <= 2.2e-15 relative (round 2: was
+// degree 6, 3.4e-18 -- the log-likelihood tolerance of 1e-9 needs ~1e-12 of a covariance entry).  N = 64, degree 4
+// (3.8e-14, one FMA less) is kept as an option: its 256 bytes more per block cost the m = 30 tier its 12th block per
+// SM (12 x (18.6 KB + 1 KB reserved) > 228 KB).  x is clamped at ~700 (result ~1e-304, never denormal).
 __device__ __forceinline__ double exp_neg(double x, const double *tab)
 {
     // clamp with one integer min on the high word (x >= 0, so the IEEE order is the integer
     // order; the low word of a clamped value is irrelevant)
     x = __hiloint2double(min(__double2hiint(x), 0x4085e000), __double2loint(x));
+#if VB_EXPTAB == 64
+    const double kf = fma(x, -92.33248261689366, 6755399441055744.0); // -64/ln2, 1.5*2^52
+    const int ki = __double2loint(kf);
+    const double kd = kf - 6755399441055744.0;
+    double r = fma(kd, -0.010830424667801708, -x);   // ln2/64 split hi (low 24 bits clear) ...
+    r = fma(kd, -2.8447437476627285e-11, r);         // ... + lo
+    double q = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    const double T = tab[ki & 63];
+    const double v = fma(T, q * r, T);
+    return __hiloint2double(__double2hiint(v) + ((ki >> 6) << 20), __double2loint(v));
+#else
     const double kf = fma(x, -46.16624130844683, 6755399441055744.0); // -32/ln2, 1.5*2^52
     const int ki = __double2loint(kf);
     const double kd = kf - 6755399441055744.0;
     double r = fma(kd, -0.021660849335603416, -x);   // ln2/32 split hi (low 24 bits clear) ...
     r = fma(kd, -5.689487495325457e-11, r);          // ... + lo (a single-FMA reduction was measured: no faster)
+#ifdef VB_EXP_DEG6
     double q = fma(r, 1.0 / 720.0, 1.0 / 120.0);
     q = fma(q, r, 1.0 / 24.0);
+#else
+    double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+#endif
     q = fma(q, r, 1.0 / 6.0);
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
-    const double T = tab[ki & (VB_EXPTAB - 1)];
+    const double T = tab[ki & 31];
     const double v = fma(T, q * r, T);
     return __hiloint2double(__double2hiint(v) + ((ki >> 5) << 20), __double2loint(v));
+#endif
 }
 
 // K_nu(x) and K_{nu-1}(x), x > 0, by Temme's method (N. M. Temme, J. Comput. Phys. 19 (1975) 324):

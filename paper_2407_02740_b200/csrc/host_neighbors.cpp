@@ -569,4 +569,26 @@ int64_t vbh_dependency_levels(const int64_t *nn, int64_t n, int mp1, int64_t *or
     return nlev;
 }
 
+// Narrow a block of neighbor indices (int64, -1 = padding) to int32 for the host-to-device transfer: the table is
+// 8(m+1) bytes per observation and the end-to-end path is bound by the PCIe copy of it; indices of any dataset with
+// n < 2^31 points fit 32 bits, the device widens them back (vb200_widen_indices).  All host threads; returns 0, or
+// 1 if some value does not fit (the caller then ships the int64 rows as they are).
+int vbh_narrow_indices(const int64_t *src, int32_t *dst, int64_t count, int workers)
+{
+    if (!src || !dst || count < 0)
+        return -1;
+    int bad = 0;
+#ifdef _OPENMP
+    if (workers < 1)
+        workers = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(workers) reduction(| : bad)
+#endif
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t v = src[i];
+        dst[i] = (int32_t)v;
+        bad |= (v != (int64_t)(int32_t)v);
+    }
+    return bad;
+}
+
 } // extern "C"

@@ -35,7 +35,8 @@
 // Experiment knobs (ablations, clock accounting, alternative schedules) are honoured only in builds made with
 // -DVB200_EXPERIMENTS (tools/build_variant.py); the product build always uses the defaults below.
 #if !defined(VB200_EXPERIMENTS) && (defined(TILED_ABLATE) || defined(TILED_STAGGER_NS) || defined(TILED_CLOCKS) || \
-                                    defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB))
+                                    defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB) || \
+                                    defined(TILED_SMEM_BLOCKS))
 #error "TILED_* experiment knobs need -DVB200_EXPERIMENTS"
 #endif
 #ifndef TILED_WPB
@@ -101,9 +102,10 @@ __device__ __forceinline__ void pair_terms_r(const EvalParams &E, const double *
         for (int l = 0; l < D; ++l)
             x2 = fma(dl[l], dl[l], x2);
         // x = sqrt(x2) = g (1 + e/2 + 3 e^2/8), g = x2 y, e = 1 - x2 y^2, y = MUFU.RSQ64H seed
+        // e from g (one FMA instead of a product and an FMA; same chain depth)
         const double y = rsqrt_seed(x2);
-        const double e = fma(-x2, y * y, 1.0);
         const double g = x2 * y;
+        const double e = fma(-g, y, 1.0);
         const double x = fma(fma(e, 0.375, 0.5), g * e, g);
 #if (TILED_ABLATE & 32)
         const double se = 1e-3 * x2; // timing experiment: no exp (11 FP64 + 6 integer instructions + 1 table load less)
@@ -220,10 +222,10 @@ struct PairSched {
 // the slot is always the column part (static offset from the lane's column base), l before it always the
 // row part (static offset from the row index); only inside the diagonal block does the side depend on the
 // lane.  `oz` is an opaque zero (see the kernel): it keeps the lane-dependent selects inside the batch loop.
-template <int G, int S, int s, int l>
+template <int G, int S, int NP, int s, int l>
 __device__ __forceinline__ double sym_packed_load(const double *M, const int colb_a, const int a, const int oz)
 {
-    using Geo = TileGeom<G, S>;
+    using Geo = TileGeom<G, S, NP>;
     if constexpr (l >= (s + 1) * G)
         return M[colb_a + l];
     else if constexpr (l < s * G)
@@ -235,7 +237,7 @@ __device__ __forceinline__ double sym_packed_load(const double *M, const int col
 }
 
 // rows a = rowi[s] of columns l0 = 2h, l0 + 1 of QD packed symmetric matrices, and the pair (u_l0, u_l0+1)
-template <int G, int S, int QD, int H, int s = 0>
+template <int G, int S, int NP, int QD, int H, int s = 0>
 __device__ __forceinline__ void sym_fetch_pair(const double *Dms, const int DSZ, const double *us, const int (&colb_r)[S],
                                                const int (&rowi)[S], const int oz, double (&dv)[2][QD][S], double2 &uv)
 {
@@ -247,29 +249,29 @@ __device__ __forceinline__ void sym_fetch_pair(const double *Dms, const int DSZ,
         for (int r = 0; r < QD; ++r) {
             dv[0][r][s] = 0.0;
             if constexpr (l0 >= 1)
-                dv[0][r][s] = sym_packed_load<G, S, s, l0>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
-            dv[1][r][s] = sym_packed_load<G, S, s, l1>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+                dv[0][r][s] = sym_packed_load<G, S, NP, s, l0>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+            dv[1][r][s] = sym_packed_load<G, S, NP, s, l1>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
         }
-        sym_fetch_pair<G, S, QD, H, s + 1>(Dms, DSZ, us, colb_r, rowi, oz, dv, uv);
+        sym_fetch_pair<G, S, NP, QD, H, s + 1>(Dms, DSZ, us, colb_r, rowi, oz, dv, uv);
     }
 }
 
 // rows a = rowi[s] of column l of QD packed symmetric matrices
-template <int G, int S, int QD, int l, int s = 0>
+template <int G, int S, int NP, int QD, int l, int s = 0>
 __device__ __forceinline__ void sym_fetch_col(const double *Dms, const int DSZ, const int (&colb_r)[S], const int (&rowi)[S],
                                               const int oz, double (&dv)[QD][S])
 {
     if constexpr (s < S) {
 #pragma unroll
         for (int r = 0; r < QD; ++r)
-            dv[r][s] = sym_packed_load<G, S, s, l>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
-        sym_fetch_col<G, S, QD, l, s + 1>(Dms, DSZ, colb_r, rowi, oz, dv);
+            dv[r][s] = sym_packed_load<G, S, NP, s, l>(Dms + r * DSZ, colb_r[s], rowi[s], oz);
+        sym_fetch_col<G, S, NP, QD, l, s + 1>(Dms, DSZ, colb_r, rowi, oz, dv);
     }
 }
 
-template <int G, int S, int D, int QD>
+template <int G, int S, int D, int QD, int NP = 1>
 struct LikSmem {
-    using Geo = TileGeom<G, S>;
+    using Geo = TileGeom<G, S, NP>;
     static constexpr int DP = (D + 1) & ~1;                 // padded coordinate stride (16-byte rows)
     static constexpr int PTS = Geo::CAP * DP;               // scaled coordinates of the local frame
     // The column store of the factorization and every D_r share ONE packing: element (a, c), a >= c,
@@ -301,14 +303,33 @@ __device__ __forceinline__ void phase_sync()
 //             (CAP = 48 / 64) and cheap around an out-of-line call (general-order Matern: the Bessel routine).
 //             Pairs that touch a padding row are not evaluated at all (the table lists live pairs first).
 // Everything after the pair phase is shared.
-template <int G, int S, int FAM, int D, int P, bool PT = false>
-__global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
+// Resident blocks per SM the kernel is compiled for (__launch_bounds__): the register tier of the geometry, but never
+// more than the instance's shared memory admits -- an instance that only fits 8 blocks (two derivative matrices:
+// space-time, general Matern, anisotropic) may then use 255 registers instead of being held to the 168 of 12 blocks.
+template <int G, int S, int D, int QD, int NP>
+__host__ __device__ constexpr int tiled_launch_blocks()
+{
+    constexpr int by_reg = tiled_min_blocks(G, S, NP);
+#if defined(TILED_SMEM_BLOCKS) && TILED_WPB == 1
+    constexpr long long bytes = (long long)LikSmem<G, S, D, QD, NP>::TOTAL * 8 + 1024; // + the per-block reservation
+    constexpr int by_smem = (int)(233472 / bytes) < 1 ? 1 : (int)(233472 / bytes);
+    return by_smem < by_reg ? by_smem : by_reg;
+#else
+    return by_reg;
+#endif
+}
+
+// NP > 1 (pair-table variant only): the first NP local rows are padding rows of every observation the instance
+// serves (m+1 <= CAP-NP); see TileGeom.
+template <int G, int S, int FAM, int D, int P, bool PT = false, int NP = 1>
+__global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, FamTraits<FAM, D>::QD, NP>() + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
 {
     static_assert(!PT || TILED_WPB == 1, "the pair-table variant runs one warp per block");
-    using Geo = TileGeom<G, S>;
+    static_assert(NP == 1 || PT, "static padding rows are implemented for the pair-table variant");
+    using Geo = TileGeom<G, S, NP>;
     using FT = FamTraits<FAM, D>;
-    constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q;
-    using SM = LikSmem<G, S, D, QD>;
+    constexpr int CAP = Geo::CAP, OPW = Geo::OPW, QD = FT::QD, Q = FT::Q, Z = Geo::Z;
+    using SM = LikSmem<G, S, D, QD, NP>;
     constexpr int DP = SM::DP, DSZ = SM::DSZ;
     constexpr int L = (1 + Q) * (2 + P + P * P) + Q * Q;
     constexpr int NACC = (L + G - 1) / G;
@@ -327,19 +348,22 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
     for (int t = threadIdx.x; t < VB_EXPTAB; t += 32 * TILED_WPB)
         etab[t] = E.sig2 * exp2((double)t * (1.0 / VB_EXPTAB));
     // never written again: diagonal and column 0 of every D_r (zero), column 0 of the column store
-    for (int a = lg; a < CAP; a += G) {
+    for (int a = Z + lg; a < CAP; a += G) {
 #pragma unroll
         for (int j = 0; j < QD; ++j) {
-            Dms[j * DSZ + a] = 0.0;
+            Dms[j * DSZ + Geo::colbase(Z) + a] = 0.0;
             Dms[j * DSZ + Geo::colbase(a) + a] = 0.0;
         }
-        KLs[a] = 0.0;
+        KLs[Geo::colbase(Z) + a] = 0.0;
     }
-    int rowi[S], colb_r[S];
+    // rowm: the row a lane ADDRESSES in the packed triangles -- its own, or (static padding rows below Z, which are
+    // not part of the packing) the padding row Z, whose entries are the zeros a padding row must read
+    int rowi[S], rowm[S], colb_r[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         rowi[s] = s * G + ((s & 1) ? (G - 1 - lg) : lg);
-        colb_r[s] = Geo::colbase(rowi[s]);
+        rowm[s] = (Z > 0) ? max(rowi[s], Z) : rowi[s];
+        colb_r[s] = Geo::colbase(rowm[s]);
     }
     double dscale[QD];
 #pragma unroll
@@ -416,9 +440,29 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         const int64_t batch = batch0 + warp;
         const int64_t i = E.i0 + batch * OPW + g;
         const bool active = i < E.i1;
-#if !TILED_PREFETCH
+#if !TILED_PREFETCH || TILED_PREFETCH >= 4
         load_idx(batch, nidx);
         load_rec(nidx, nrec);
+#if TILED_PREFETCH >= 4
+        // register-free: the index row of this warp's NEXT batch is requested into L2 (4) / L1 (6) now
+        {
+            const int64_t inx = i + stride * OPW;
+            if (inx < E.i1) {
+                const int64_t *nrow = E.nn + (inx - E.nn_row0) * E.mp1;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int col = CAP - 1 - rowi[s];
+                    if (col < E.mp1) {
+#if TILED_PREFETCH == 6
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(nrow + col));
+#else
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + col));
+#endif
+                    }
+                }
+            }
+        }
+#endif
 #elif TILED_PREFETCH == 2
         load_rec(nidx, nrec); // indices arrived one batch ago, the records were prefetched into L1 / L2
 #endif
@@ -463,7 +507,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             // diagonal block of the slot: the diagonal entry, zeros above it (never used, must be finite)
             const double dg = live ? E.diag : 1.0;
             if constexpr (PT) {
-                KLs[colb_r[s] + a] = dg;
+                if (Z == 0 || a >= Z)
+                    KLs[colb_r[s] + a] = dg;
             } else {
 #pragma unroll
                 for (int c = s * G; c < (s + 1) * G; ++c)
@@ -498,7 +543,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         if constexpr (PT) {
             // ---- pair-table pair phase.  The table lists the off-diagonal pairs (a > c) by DESCENDING c, so the
             //      k(k-1)/2 pairs among the live points come first; the rest is zero-filled. ----
-            using TS = TileSmem<G, S, D, QD>;
+            using TS = TileSmem<G, S, D, QD, NP>;
             // pairs in flight per lane: two for the closed forms; ONE for the general Matern, whose Bessel evaluations
             // are long enough to spill when two are interleaved (measured 38 ms against 50 ms per evaluation)
             constexpr int NI = (FAM == FAM_MATERN) ? 1 : TS::NI;
@@ -557,8 +602,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #pragma unroll
             for (int s = 0; s < S; ++s)
 #pragma unroll
-                for (int c = 0; c < (s + 1) * G; ++c)
-                    Kr[s][c] = KLs[Geo::colbase(c) + rowi[s]];
+                for (int c = Z; c < (s + 1) * G; ++c)
+                    Kr[s][c] = KLs[Geo::colbase(c) + rowm[s]];
         } else {
             using PS = PairSched<G, S>;
             constexpr int NI = TILED_RNI;
@@ -709,11 +754,11 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             }
         };
         if (!(TILED_ABLATE & 2)) {
-        publish(1); // local row 0 is always padding: step 0 is the identity
-        multipliers(1);
+        publish(NP); // local rows 0 .. NP-1 are always padding: their steps are the identity
+        multipliers(NP);
         }
         if (!(TILED_ABLATE & 2))
-        static_for<1, CAP - 1>([&](auto jc) {
+        static_for<NP, CAP - 1>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
             constexpr int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
             const double *col = KLs + Geo::colbase(j);
@@ -800,8 +845,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const int a = rowi[s];
-                const double da = (a == CAP - 1) ? d_e : KLs[colb_r[s] + a];
-                const bool real = a >= 1;                       // local row 0: identity padding (store holds 0)
+                const double da = (a == CAP - 1) ? d_e : KLs[colb_r[s] + rowm[s]];
+                const bool real = a >= NP;                      // static padding rows: identity (the store holds 0)
                 invd[s] = !real ? 1.0 : ((a == CAP - 1) ? rho_e : rcp_pos3(da));
                 badm[s] = __ballot_sync(FULLMASK, real && da <= E.piv_floor);
                 if (G < 32)
@@ -858,19 +903,19 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                     if (s * G < l) // slot has rows < l
                         Kl[s] = KLs[colb_r[s] + l];
             };
-            if (lg == 0)
-                us[0] = 0.0;
+            if (lg < NP)
+                us[lg] = 0.0;
             if (!(TILED_ABLATE & 4)) {
                 static_for<0, BD>([&](auto ic) {
                     constexpr int l = CAP - 1 - decltype(ic)::value;
-                    if constexpr (l >= 1) {
+                    if constexpr (l >= NP) {
                         fetchK(l, Kq[decltype(ic)::value % BD]);
 #if TILED_FUSE_DU
-                        sym_fetch_col<G, S, QD, l>(Dms, DSZ, colb_r, rowi, oz, Dq[decltype(ic)::value % BD]);
+                        sym_fetch_col<G, S, NP, QD, l>(Dms, DSZ, colb_r, rowm, oz, Dq[decltype(ic)::value % BD]);
 #endif
                     }
                 });
-                static_for<0, CAP - 1>([&](auto ic) {
+                static_for<0, CAP - NP>([&](auto ic) {
                     constexpr int it = decltype(ic)::value, l = CAP - 1 - it;
                     constexpr int sl = l / G, ol = (sl & 1) ? (G - 1 - l % G) : (l % G);
                     const double ul = __shfl_sync(FULLMASK, fma(-sb[sl], invd[sl], eb[sl]), ol, G);
@@ -887,10 +932,10 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                         for (int r = 0; r < QD; ++r)
                             rr[r][s] = fma(Dq[it % BD][r][s], ul, rr[r][s]);
 #endif
-                    if constexpr (l - BD >= 1) {
+                    if constexpr (l - BD >= NP) {
                         fetchK(l - BD, Kq[it % BD]);
 #if TILED_FUSE_DU
-                        sym_fetch_col<G, S, QD, l - BD>(Dms, DSZ, colb_r, rowi, oz, Dq[it % BD]);
+                        sym_fetch_col<G, S, NP, QD, l - BD>(Dms, DSZ, colb_r, rowm, oz, Dq[it % BD]);
 #endif
                     }
                 });
@@ -926,7 +971,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
             static_for<0, DD>([&](auto hc) {
                 constexpr int h = decltype(hc)::value;
                 if constexpr (h < NH)
-                    sym_fetch_pair<G, S, QD, h>(Dms, DSZ, us, colb_r, rowi, oz, dq[h % DD], uq[h % DD]);
+                    sym_fetch_pair<G, S, NP, QD, h>(Dms, DSZ, us, colb_r, rowm, oz, dq[h % DD], uq[h % DD]);
             });
             static_for<0, NH>([&](auto hc) {
                 constexpr int h = decltype(hc)::value;
@@ -940,7 +985,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
                     }
                 const double2 uv = uq[h % DD];
                 if constexpr (h + DD < NH)
-                    sym_fetch_pair<G, S, QD, h + DD>(Dms, DSZ, us, colb_r, rowi, oz, dq[h % DD], uq[h % DD]);
+                    sym_fetch_pair<G, S, NP, QD, h + DD>(Dms, DSZ, us, colb_r, rowm, oz, dq[h % DD], uq[h % DD]);
 #pragma unroll
                 for (int s = 0; s < S; ++s)
 #pragma unroll
@@ -961,7 +1006,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         PHASE_MARK(3);
         // ---- [tt_1..tt_QD, ut] through Lt^-1 (unit-diagonal forward sweeps on the register-resident rows) ----
 #pragma unroll
-        for (int j = 1; j < ((TILED_ABLATE & 8) ? 1 : CAP - 1); ++j) {
+        for (int j = NP; j < ((TILED_ABLATE & 8) ? NP : CAP - 1); ++j) {
             const int sj = j / G;
             const int oj = (sj & 1) ? (G - 1 - j % G) : (j % G);
             double Lm[S]; // multipliers of column j, stored masked (exactly 0 for rows <= j) by the factorization
@@ -1007,6 +1052,17 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
         for (int s = 0; s < S; ++s)
             if (nidx[s] >= 0)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(E.rec + nidx[s] * E.rs));
+#elif TILED_PREFETCH == 5
+        // the next batch's indices come from L2 by now (requested at the top of this batch); its records are
+        // requested into L1 and the indices dropped again (nothing is held across the batch boundary)
+        {
+            int64_t pidx[S];
+            load_idx(batch + stride, pidx);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (pidx[s] >= 0)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(E.rec + pidx[s] * E.rs));
+        }
 #endif
         const double sq = rsqrt_pos(d_e); // s = 1/sqrt(d_e)
         const double ze = __shfl_sync(FULLMASK, rhs[0][se], oe, G) * sq;
@@ -1134,6 +1190,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_min_blocks(G, S) + TILE
 // ---------------------------------------------------------------------------
 struct TiledInstance {
     int g, s, cap, family, d, p, wpb;
+    int npad; // leading local rows that are padding for every observation served: m+1 <= cap - npad
     int pair_table; // 1: the pair-table pair phase (PT = true) -- needs EvalParams::pair_tab
     void (*kernel)(const EvalParams);
     int smem_doubles;
@@ -1142,14 +1199,23 @@ struct TiledInstance {
 
 #define TILED_INST(G_, S_, FAM_, D_, P_)                                                                        \
     {                                                                                                           \
-        G_, S_, (G_) * (S_), FAM_, D_, P_, TILED_WPB, 0, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                                  \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, TILED_WPB, 1, 0, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_>,                               \
             LikSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                 \
             "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ">"                            \
     }
 
 #define TILED_INST_PT(G_, S_, FAM_, D_, P_)                                                                     \
     {                                                                                                           \
-        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, 1, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_, true>,              \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, 1, 1, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_, true>,           \
             LikSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD>::TOTAL,                                                \
             "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ",pair-table>"               \
+    }
+
+// pair-table variant with NP_ static padding rows: serves m+1 <= G_*S_ - NP_ with the shared memory of a
+// (G_*S_ - NP_ + 1)-row tier
+#define TILED_INST_PTN(G_, S_, FAM_, D_, P_, NP_)                                                               \
+    {                                                                                                           \
+        G_, S_, (G_) * (S_), FAM_, D_, P_, 1, NP_, 1, vecchia_tiled_kernel<G_, S_, FAM_, D_, P_, true, NP_>,    \
+            LikSmem<G_, S_, D_, FamTraits<FAM_, D_>::QD, NP_>::TOTAL,                                           \
+            "vecchia_tiled_kernel<G=" #G_ ",S=" #S_ "," #FAM_ ",D=" #D_ ",P=" #P_ ",pair-table,NP=" #NP_ ">"    \
     }

@@ -87,23 +87,29 @@ __device__ __forceinline__ void pair_terms_s(const EvalParams &E, const double *
     }
 }
 
-template <int G, int S>
+// NP = number of leading local rows that are padding rows for EVERY observation the tier serves (m+1 <= CAP-NP).
+// Rows 0 .. NP-2 never touch shared memory; row Z = NP-1 is the one padding row the packing keeps (its column and
+// diagonal entries hold zeros), so a tier with NP > 1 packs a (CAP-Z) x (CAP-Z) triangle: less shared memory per
+// observation, i.e. more resident warps, and the factorization / sweeps start at column NP.
+template <int G, int S, int NP = 1>
 struct TileGeom {
     static constexpr int CAP = G * S;
+    static constexpr int Z = NP - 1;                   // first local row present in the packed triangles
+    static constexpr int CAPE = CAP - Z;               // rows of the packed triangles
     static constexpr int OPW = 32 / G;                 // observations per warp
-    static constexpr int TRI = CAP * (CAP + 1) / 2;    // packed lower triangle incl. diagonal
-    // column store: element (c, j), c >= j, of the (unscaled) factor lives at colbase(j) + c, columns
-    // packed back to back.  colbase(j) = -j(j+1)/2 (mod 16) when CAP = 32, so the 16 lanes of a group
+    static constexpr int TRI = CAPE * (CAPE + 1) / 2;  // packed lower triangle incl. diagonal
+    // column store: element (c, j), c >= j >= Z, of the (unscaled) factor lives at colbase(j) + c, columns
+    // packed back to back.  colbase(j) = -j(j+1)/2 (mod 16) when CAP = 32, NP = 1, so the 16 lanes of a group
     // reading "their" columns at a common row hit 16 different 8-byte banks.
-    __host__ __device__ static constexpr int colbase(int j) { return j * (CAP - 1) - j * (j - 1) / 2; }
-    static constexpr int KL = TRI + 2; // one element past the last column may be read by a pair load
+    __host__ __device__ static constexpr int colbase(int j) { return (j - Z) * (CAPE - 1) - (j - Z) * (j - Z - 1) / 2 - Z; }
+    static constexpr int KL = (TRI + 3) & ~1; // one element past the last column may be read by a pair load
     __host__ __device__ static constexpr int slot_of(int r) { return r / G; }
     __host__ __device__ static constexpr int lane_of(int r) { return ((r / G) & 1) ? (G - 1 - r % G) : (r % G); }
 };
 
-template <int G, int S, int D, int QD>
+template <int G, int S, int D, int QD, int NP = 1>
 struct TileSmem {
-    using Geo = TileGeom<G, S>;
+    using Geo = TileGeom<G, S, NP>;
     static constexpr int DP = (D + 1) & ~1;                 // padded coordinate stride (16-byte rows)
     static constexpr int PTS = Geo::CAP * DP;               // scaled coordinates of the local frame
     // K staging, the column store of the factorization and every D_j share ONE packing: element
@@ -113,17 +119,17 @@ struct TileSmem {
     static constexpr int DSZ = (Geo::TRI + 1) & ~1;
     static constexpr int PER_OBS = PTS + Geo::KL + QD * DSZ;
     static constexpr int TOTAL = VB_EXPTAB + Geo::OPW * PER_OBS;
-    // Local row 0 is ALWAYS a padding row (tiers serve m+1 <= CAP-1), so nothing is computed for it.
+    // Local rows 0 .. NP-1 are ALWAYS padding rows (tiers serve m+1 <= CAP-NP), so nothing is computed for them.
     // off-diagonal pair table (device memory, shared by all blocks): TOFF entries padded to a
     // multiple of NI*G with copies of the last pair; entry = a << 24 | c << 16 | (colbase(c) + a)
-    static constexpr int TOFF = (Geo::CAP - 1) * (Geo::CAP - 2) / 2; // pairs among local rows 1..CAP-1
+    static constexpr int TOFF = (Geo::CAP - NP) * (Geo::CAP - NP - 1) / 2; // pairs among local rows NP..CAP-1
     static constexpr int NI = TILED_NI;                     // pairs in flight per lane in the pair loop
     static constexpr int TPAD = (TOFF + NI * G - 1) / (NI * G) * (NI * G);
 };
 
 // blocks per SM (one warp per block) the register budget of a tier is tuned for: the rows a lane
 // keeps in registers take G*S(S+1) 32-bit registers; 168 registers = 3 warps per SM sub-partition
-__host__ __device__ constexpr int tiled_min_blocks(int G, int S)
+__host__ __device__ constexpr int tiled_min_blocks(int G, int S, int NP = 1)
 {
 #ifdef TILED_MINB
     return TILED_MINB; // development knob

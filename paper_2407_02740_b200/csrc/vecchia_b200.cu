@@ -895,7 +895,7 @@ extern "C" int vb200_tiled_instance(int k, int *g, int *s, int *cap, int *family
             const TiledInstance &t = part.items[k];
             if (g) *g = t.g;
             if (s) *s = t.s;
-            if (cap) *cap = t.cap;
+            if (cap) *cap = t.cap - (t.npad - 1); // serves m+1 <= *cap - 1
             if (family) *family = t.family;
             if (d) *d = t.d;
             if (p) *p = t.p;

@@ -33,7 +33,9 @@ def main():
     lines = [f'#include "{a.header}"', "", "extern const TiledInstance kTiledPart0[] = {"]
     for it in items:
         m = macro
-        if len(it) == 6:
+        if len(it) == 7:    # g,s,fam,d,p,TILED_INST_PTN,np
+            m, it = it[5], it[:5] + it[6:]
+        elif len(it) == 6:
             m, it = it[5], it[:5]
         lines.append(f"    {m}({', '.join(it)}),")
     lines += ["};", f"extern const int kTiledPart0Count = {len(items)};", ""]
