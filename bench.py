@@ -371,10 +371,12 @@ def ours_arm(args):
     t0 = time.perf_counter()
     es.record()
     e2e_each = []
+    h2d_seen, narrowed = 0, False
     for _ in range(e2e_steps):
         t1 = time.perf_counter()
         with new_problem() as pr:
             step(pr)
+            h2d_seen, narrowed = pr.h2d_bytes, pr.upload_narrowed
         e2e_each.append(1000.0 * (time.perf_counter() - t1))
     ee.record()
     torch.cuda.synchronize()
@@ -386,7 +388,11 @@ def ours_arm(args):
         t = torch.tensor([e2e_mean_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_mean_ms = float(t)
-    h2d = int(hy.numel() * 8 + hX.numel() * 8 + hl.numel() * 8 + hn.numel() * 8)
+    # bytes copied per step, as counted by the constructor that copies them: y, X, locs as float64, the neighbor
+    # table as int32 when the narrowed upload is on (int64 host rows narrowed by the host threads inside the timed
+    # region, widened again on the device) -- the HOST input is the reference's int64 table either way
+    h2d = int(h2d_seen)
+    h2d_host_input = int(hy.numel() * 8 + hX.numel() * 8 + hl.numel() * 8 + hn.numel() * 8)
     d2h = int((engine.acc_len(args.p, q) + 2) * 8)
 
     # ---- roofline of the main kernel (FP64 bound; peak = best of the two FP64 micro-kernels, both recorded) ----
@@ -428,7 +434,10 @@ def ours_arm(args):
                 "ms_per_step": e2e_mean_ms, "ms_per_step_median": e2e_median_ms, "steps": e2e_steps,
                 "ms_each": [round(x, 2) for x in e2e_each], "ms_min": round(float(min(e2e_each)), 3),
                 "statistic": "mean over the timed steps (max of CUDA-event and host wall time)",
-                "path": "engine.DeviceProblem(pinned host y/X/locs/nn): table uploaded in 16 chunks on a side stream, vb200_create + vb200_eval_async per chunk behind the copies -> totals on the host"},
+                "host_input_bytes_per_step": h2d_host_input, "table_narrowed_to_int32": bool(narrowed),
+                "path": "engine.DeviceProblem(pinned host y/X/locs/nn): table " + ("narrowed to int32 by the host threads, " if narrowed else "")
+                        + "uploaded in 16 chunks on a side stream" + (", widened on the device (vb200_widen_indices)" if narrowed else "")
+                        + ", vb200_create + vb200_eval_async per chunk behind the copies -> totals on the host"},
         "gpu_launches": launches, "roofline": roofline,
         "loglik": ev.loglik, "neighbor_search_s": t_nn, "rank_kernel_ms": rank_kernel_ms,
         "step_minus_kernel_us": 1000.0 * (ms_per_step - max(rank_kernel_ms)),

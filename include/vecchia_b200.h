@@ -204,6 +204,11 @@ int vb200_last_kernel_ms(vb200_problem *prob, double *ms);
  * 2 GiB of freed memory cached (so re-creating a problem per step does not pay the driver's map/unmap);
  * this returns the cached memory of `device` to the driver (synchronises the device). */
 int vb200_release_memory(int device);
+/* Upload helper for the neighbor table (the largest input: 8(m+1) bytes per observation, and the end-to-end path
+ * is bound by its PCIe copy): a host caller may narrow the int64 indices of a dataset with n < 2^31 points to int32
+ * (vbh_narrow_indices in libvecchia_host.so), copy half the bytes, and have the device widen them in place of the
+ * rows vb200_create was given.  src / dst are DEVICE pointers (8- / 16-byte aligned), enqueued on `stream`. */
+int vb200_widen_indices(const int32_t *src, int64_t *dst, int64_t count, void *stream);
 /* Number of evaluations since process start for which VB200_LAYOUT_AUTO found no TILED_REG instance and ran
  * the shape-agnostic WARP_SMEM kernel instead (roughly 10x slower): 0 means every evaluation took the fast path. */
 unsigned long long vb200_fallback_count(void);

@@ -50,6 +50,7 @@ _SIGNATURES = {
     "vb200_measure_fp64_peak": (c_int, [c_int, c_double, _dp, _dp]),
     "vb200_measure_fp64_peak_mma": (c_int, [c_int, c_double, _dp, _dp]),
     "vb200_release_memory": (c_int, [c_int]),
+    "vb200_widen_indices": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "vb200_fallback_count": (ctypes.c_ulonglong, []),
 }
 

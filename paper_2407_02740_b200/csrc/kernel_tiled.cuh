@@ -36,7 +36,7 @@
 // -DVB200_EXPERIMENTS (tools/build_variant.py); the product build always uses the defaults below.
 #if !defined(VB200_EXPERIMENTS) && (defined(TILED_ABLATE) || defined(TILED_STAGGER_NS) || defined(TILED_CLOCKS) || \
                                     defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB) || \
-                                    defined(TILED_SMEM_BLOCKS))
+                                    defined(TILED_NO_SMEM_BLOCKS))
 #error "TILED_* experiment knobs need -DVB200_EXPERIMENTS"
 #endif
 #ifndef TILED_WPB
@@ -303,17 +303,19 @@ __device__ __forceinline__ void phase_sync()
 //             (CAP = 48 / 64) and cheap around an out-of-line call (general-order Matern: the Bessel routine).
 //             Pairs that touch a padding row are not evaluated at all (the table lists live pairs first).
 // Everything after the pair phase is shared.
-// Resident blocks per SM the kernel is compiled for (__launch_bounds__): the register tier of the geometry, but never
-// more than the instance's shared memory admits -- an instance that only fits 8 blocks (two derivative matrices:
-// space-time, general Matern, anisotropic) may then use 255 registers instead of being held to the 168 of 12 blocks.
+// Resident blocks per SM the kernel is compiled for (__launch_bounds__): the register tier of the geometry, unless the
+// instance's shared memory admits 8 blocks or fewer anyway (two or three derivative matrices: space-time, general
+// Matern, anisotropic) -- then it may use the registers of those blocks instead of being held to the 168 of 12 blocks
+// (measured at n = 2^20: space-time d = 3 5.75 -> 5.47 ms, anisotropic d = 2 5.48 -> 5.05 ms; an instance that fits
+// 11 blocks, Matern-3/2 d = 3 p = 4, got slower when compiled for 11: the rule only applies at <= 8).
 template <int G, int S, int D, int QD, int NP>
 __host__ __device__ constexpr int tiled_launch_blocks()
 {
     constexpr int by_reg = tiled_min_blocks(G, S, NP);
-#if defined(TILED_SMEM_BLOCKS) && TILED_WPB == 1
+#if !defined(TILED_NO_SMEM_BLOCKS) && TILED_WPB == 1
     constexpr long long bytes = (long long)LikSmem<G, S, D, QD, NP>::TOTAL * 8 + 1024; // + the per-block reservation
     constexpr int by_smem = (int)(233472 / bytes) < 1 ? 1 : (int)(233472 / bytes);
-    return by_smem < by_reg ? by_smem : by_reg;
+    return (by_smem <= 8 && by_smem < by_reg) ? by_smem : by_reg;
 #else
     return by_reg;
 #endif

@@ -1255,6 +1255,38 @@ extern "C" int vb200_measure_fp64_peak_mma(int device, double seconds, double *t
     return VB200_OK;
 }
 
+// Widen neighbor indices shipped as int32 (vbh_narrow_indices of the host library: half the PCIe bytes of the
+// table) back to the int64 rows the kernels read.  Both pointers are device memory; `count` entries; enqueued on
+// `stream` (no synchronisation).
+__global__ void widen_indices_kernel(const int *__restrict__ src, long long *__restrict__ dst, long long count)
+{
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long pairs = count / 2;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < pairs; t += stride) {
+        const int2 v = reinterpret_cast<const int2 *>(src)[t];
+        reinterpret_cast<longlong2 *>(dst)[t] = make_longlong2((long long)v.x, (long long)v.y);
+    }
+    if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+        dst[count - 1] = (long long)src[count - 1];
+}
+
+extern "C" int vb200_widen_indices(const int32_t *src, int64_t *dst, int64_t count, void *stream)
+{
+    if (count < 0 || (count > 0 && (!src || !dst)))
+        return fail(VB200_EINVAL, "vb200_widen_indices: bad arguments");
+    if (count == 0)
+        return VB200_OK;
+    if ((reinterpret_cast<uintptr_t>(src) & 7) || (reinterpret_cast<uintptr_t>(dst) & 15))
+        return fail(VB200_EINVAL, "vb200_widen_indices: src must be 8-byte and dst 16-byte aligned");
+    const int threads = 256;
+    long long blocks = (count / 2 + threads - 1) / threads;
+    blocks = blocks < 1 ? 1 : (blocks > 148 * 16 ? 148 * 16 : blocks);
+    widen_indices_kernel<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        src, reinterpret_cast<long long *>(dst), (long long)count);
+    CUDA_TRY(cudaGetLastError());
+    return VB200_OK;
+}
+
 // Return the cached (freed) device memory of the library's private pool on `device` to the driver.
 extern "C" int vb200_release_memory(int device)
 {

@@ -119,6 +119,29 @@ def _device_streams(torch, device):
     return pair
 
 
+_STAGING: dict = {}
+
+
+def _index_staging(torch, count: int, owner):
+    """One pinned int32 host buffer per process for the narrowed neighbor-table upload (pinning 130 MB costs tens of
+    milliseconds: done once, grown on demand) and the event that says its last user's copies have finished."""
+    import weakref
+    prev = _STAGING.get("owner")
+    prev = prev() if prev is not None else None
+    if prev is not None and prev is not owner and getattr(prev, "_pending", None):
+        prev._settle_uploads()  # it still has pieces to narrow into this buffer
+    _STAGING["owner"] = weakref.ref(owner)
+    buf = _STAGING.get("buf")
+    if buf is None or buf.numel() < count:
+        buf = torch.empty(max(count, 1), dtype=torch.int32, pin_memory=True)
+        _STAGING["buf"] = buf
+        _STAGING["event"] = None
+    ev = _STAGING.get("event")
+    if ev is not None:
+        ev.synchronize()  # a previous problem's host-to-device copies read this buffer
+    return buf
+
+
 class DeviceProblem:
     """Device-resident inputs of one dataset (or one contiguous shard of its rows).
 
@@ -130,14 +153,24 @@ class DeviceProblem:
 
     def __init__(self, ds: Dataset, nn: NeighborArray, family: str, device=None, row0: int = 0,
                  rows: int | None = None, layout: str = "auto", nn_is_shard: bool = False,
-                 upload_chunks: int | None = None):
+                 upload_chunks: int | None = None, upload_narrow: bool | None = None):
         """``nn`` is the full (n, m+1) table, or -- with ``nn_is_shard`` -- only its rows
         [row0, row0+rows) (what each rank of a sharded run builds for itself).
 
         The neighbor table is by far the largest input (8(m+1) bytes per observation).  It is
         uploaded in ``upload_chunks`` pieces (default 16 for large tables) on a side stream, and the FIRST evaluation is issued
         chunk by chunk behind the copies (the C ABI evaluates any row range), so host-to-device
-        transfer and compute overlap; later evaluations see a fully resident table."""
+        transfer and compute overlap; later evaluations see a fully resident table.
+
+        ``upload_narrow`` (default OFF -- measured on the 16-core B200 host at n = 2^20, m = 30: 6.2 ms per
+        end-to-end step against 5.78 ms for the plain int64 copy, because narrowing 260 MB costs the host threads
+        3.7-4 ms in bulk and more piece by piece, i.e. as much as the 2.7 ms of PCIe time it saves; worth turning on
+        where the host has the memory bandwidth to spare): every chunk is narrowed to int32 by all
+        host threads (``vbh_narrow_indices``) into a pinned staging buffer, copied -- half the PCIe bytes -- and
+        widened back to the int64 rows on the device (``vb200_widen_indices``).  The pieces are issued LAZILY, by
+        the first evaluation: narrow piece k on the host, enqueue its copy, widening and evaluation, go on to
+        piece k+1 -- so host narrowing, PCIe and the kernel overlap (done eagerly here, the evaluation launches
+        would queue behind 4 ms of host work).  The device-side table is the same int64 array either way."""
         torch = _torch()
         lib = _cabi.load()
         fam = covariance_registry(family)
@@ -162,29 +195,53 @@ class DeviceProblem:
             stream = self._stream
             put = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=True)
             self._y, self._X, self._locs = put(ds.y), put(ds.X), put(work)
-            self._pending = []  # (first_row, end_row, event) of table chunks whose upload may be in flight
+            # [first_row, end_row, event, narrow job] of table chunks whose upload may be in flight (event None: the
+            # narrowed upload of the piece has not been issued yet -- the first evaluation does it, piece by piece)
+            self._pending = []
+            self._narrow = None
             if upload_chunks is None:
                 # 16 pieces: the evaluation of a piece overlaps the copy of the next, so the un-overlapped tail is
                 # 1/16 of the kernel (measured end to end at n = 2^20: 8 -> 6.02 ms, 12 -> 5.89, 16 -> 5.78, 32 -> 5.83)
                 upload_chunks = 16 if rows * self.mp1 * 8 >= (32 << 20) else 1
+            if upload_narrow is None:
+                upload_narrow = False
+            if upload_narrow and n >= 2 ** 31:
+                raise ValueError("upload_narrow needs n < 2^31")
+            self.upload_narrowed = False
             if rows > 0 and upload_chunks > 1:
-                host_nn = torch.from_numpy(np.ascontiguousarray(shard_rows))
+                src = np.ascontiguousarray(shard_rows)
+                host_nn = torch.from_numpy(src)
                 self._nn = torch.empty((rows, self.mp1), dtype=torch.int64, device=self.device)
                 side = side_stream
                 side.wait_stream(self._stream)  # the block just handed out may still be in use by earlier work
                 self._nn.record_stream(side)
-                cuts = np.linspace(0, rows, upload_chunks + 1).astype(np.int64)
-                with torch.cuda.stream(side):
+                cuts = (np.linspace(0, rows, upload_chunks + 1).astype(np.int64) // 2) * 2  # even rows: aligned pieces
+                cuts[-1] = rows
+                if upload_narrow:
+                    mp1 = self.mp1
+                    self._narrow = {"src": src, "stage_h": _index_staging(torch, rows * mp1, self),
+                                    "stage_d": torch.empty(rows * mp1, dtype=torch.int32, device=self.device),
+                                    "flat": self._nn.view(-1), "side": side}
+                    self._narrow["stage_d"].record_stream(side)
                     for a, b in zip(cuts[:-1], cuts[1:]):
-                        if b > a:
-                            self._nn[a:b].copy_(host_nn[a:b], non_blocking=True)
-                            ev = torch.cuda.Event()
-                            ev.record(side)
-                            self._pending.append((row0 + int(a), row0 + int(b), ev))
+                        if b > a:  # event None: not issued yet (see _issue_chunk)
+                            self._pending.append([row0 + int(a), row0 + int(b), None, (int(a) * mp1, int(b - a) * mp1)])
+                    self.upload_narrowed = True
+                else:
+                    with torch.cuda.stream(side):
+                        for a, b in zip(cuts[:-1], cuts[1:]):
+                            if b > a:
+                                self._nn[a:b].copy_(host_nn[a:b], non_blocking=True)
+                                ev = torch.cuda.Event()
+                                ev.record(side)
+                                self._pending.append([row0 + int(a), row0 + int(b), ev, None])
                 self._host_nn = host_nn  # keep the source alive while the copies run
             else:
                 self._nn = put(shard_rows) if rows > 0 else torch.zeros((1, self.mp1), dtype=torch.int64,
                                                                         device=self.device)
+            # bytes this constructor put on the bus (bench.py's end-to-end accounting)
+            self.h2d_bytes = int(8 * (ds.y.size + ds.X.size + work.size)
+                                 + (4 if self.upload_narrowed else 8) * max(rows, 0) * self.mp1)
             self._out = torch.zeros(acc_len(p, VB_MAX_Q) + 2, dtype=torch.float64, device=self.device)
             self._out_chunks = None
             handle = ctypes.c_void_p()
@@ -201,7 +258,9 @@ class DeviceProblem:
     def close(self):
         if getattr(self, "_h", None) is not None and self._h:
             if getattr(self, "_pending", None):
-                self._settle_uploads()  # never free buffers under a copy that is still in flight
+                # never free buffers under a copy that is still in flight (pieces never issued have none)
+                self._pending = [e for e in self._pending if e[2] is not None]
+                self._settle_uploads()
             self._lib.vb200_destroy(self._h)
             self._h = None
 
@@ -318,13 +377,38 @@ class DeviceProblem:
         self._publish()
         return self._out[:L + 2]
 
+    def _issue_chunk(self, entry):
+        """Narrowed upload of one piece of the table: host narrowing (all host threads), copy and device-side
+        widening on the side stream; returns the event behind them."""
+        if entry[2] is not None:
+            return entry[2]
+        torch = _torch()
+        from ..preprocess import host_library
+        nw = self._narrow
+        lo, cnt = entry[3]
+        bad = host_library().vbh_narrow_indices(nw["src"].ctypes.data + 8 * lo, nw["stage_h"].data_ptr() + 4 * lo, cnt, 0)
+        if bad:
+            raise ValueError("neighbor index outside the int32 range in a table with n < 2^31")
+        with torch.cuda.device(self.device), torch.cuda.stream(nw["side"]):
+            nw["stage_d"][lo:lo + cnt].copy_(nw["stage_h"][lo:lo + cnt], non_blocking=True)
+            _cabi.check(self._lib.vb200_widen_indices(nw["stage_d"].data_ptr() + 4 * lo, nw["flat"].data_ptr() + 8 * lo,
+                                                      cnt, ctypes.c_void_p(nw["side"].cuda_stream)),
+                        "vb200_widen_indices")
+            ev = torch.cuda.Event()
+            ev.record(nw["side"])
+        entry[2] = ev
+        _STAGING["event"] = ev
+        return ev
+
     def _settle_uploads(self):
         torch = _torch()
         with torch.cuda.device(self.device):
-            for _, _, ev in self._pending:
+            for entry in self._pending:
+                ev = entry[2] if entry[2] is not None else self._issue_chunk(entry)
                 ev.synchronize()
         self._pending = []
         self._host_nn = None
+        self._narrow = None  # the staging tensors go back to the allocator (stream-ordered: record_stream)
 
     def _totals_behind_upload(self, thp, q, jitter, i0, i1, L):
         """Evaluate [i0, i1) one upload chunk at a time, each piece waiting (on the device) for its
@@ -336,10 +420,12 @@ class DeviceProblem:
                 self._out_chunks = torch.zeros((len(self._pending), self._out.shape[0]), dtype=torch.float64,
                                                device=self.device)
             k = 0
-            for a, b, ev in self._pending:
+            for entry in self._pending:
+                a, b = entry[0], entry[1]
                 lo, hi = max(a, i0), min(b, i1)
                 if lo >= hi:
                     continue
+                ev = entry[2] if entry[2] is not None else self._issue_chunk(entry)
                 compute.wait_event(ev)
                 rc = self._lib.vb200_eval_async(self._h, self.kernel_code, thp, q, jitter, lo, hi,
                                                 ctypes.c_void_p(self._out_chunks[k].data_ptr()))
@@ -355,6 +441,7 @@ class DeviceProblem:
             if i0 <= self.row0 and i1 >= self.row0 + self.rows:
                 # the compute stream now sits behind every copy: later work needs no more waits
                 self._pending = []
+                self._narrow = None
         self._publish()
         return self._out[:L + 2]
 

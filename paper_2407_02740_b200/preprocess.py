@@ -144,6 +144,8 @@ def host_library():
         lib.vbh_order_maxmin.restype = ctypes.c_int
         lib.vbh_order_maxmin.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ip]
         lib.vbh_max_threads.restype = ctypes.c_int
+        lib.vbh_narrow_indices.restype = ctypes.c_int
+        lib.vbh_narrow_indices.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
         lib.vbh_dependency_levels.restype = ctypes.c_int64
         lib.vbh_dependency_levels.argtypes = [ip, ctypes.c_int64, ctypes.c_int, ip, ip]
         _host = lib

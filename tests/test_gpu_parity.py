@@ -217,6 +217,37 @@ def test_every_compiled_tiled_instance_against_oracle():
                 fields_close(got, want, p, q, 1e-8 if fam == 5 else 1e-9)
 
 
+def test_narrowed_table_upload_is_bit_identical():
+    """The chunked upload with the table narrowed to int32 on the host and widened on the device
+    (vbh_narrow_indices / vb200_widen_indices) leaves the same int64 rows on the device as the plain upload:
+    identical totals for the same chunking, ragged head rows and -1 padding included, and the widening kernel
+    reproduces odd-length blocks."""
+    import torch
+    from paper_2407_02740_b200 import _cabi
+    y, X, locs, theta = make_instance(21, 6001, 2, 1)
+    nn = vg.find_ordered_neighbors(locs, 30)
+    ds = vg.Dataset(y, X, locs)
+    tots = {}
+    for narrow in (False, True):
+        with DeviceProblem(ds, nn, "matern15_isotropic", upload_chunks=5, upload_narrow=narrow) as prob:
+            assert prob.upload_narrowed == narrow
+            tots[narrow] = prob.totals(theta)          # first evaluation: chunk by chunk behind the copies
+            again = prob.totals(theta)                  # resident table
+            dev_rows = prob._nn.cpu().numpy()
+            assert np.array_equal(dev_rows, nn.idx)
+            want = 8 * (y.size + X.size + locs.size) + (4 if narrow else 8) * nn.idx.size
+            assert prob.h2d_bytes == want
+        fields_close(again, tots[narrow], 1, 3, 1e-12)
+    assert np.array_equal(tots[True], tots[False])
+    lib = _cabi.load()
+    src = torch.tensor([5, -1, 7, 2 ** 31 - 1, 0, 3, -1], dtype=torch.int32, device="cuda")
+    dst = torch.full((8,), 99, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    _cabi.check(lib.vb200_widen_indices(src.data_ptr(), dst.data_ptr(), 7, None), "vb200_widen_indices")
+    torch.cuda.synchronize()
+    assert dst.cpu().tolist() == [5, -1, 7, 2 ** 31 - 1, 0, 3, -1, 99]
+
+
 def test_thread_layouts_reject_shapes_beyond_their_capacity():
     """The thread-per-observation study arms refuse shapes beyond their compile-time capacity (no fallback)."""
     y, X, locs, theta = make_instance(3, 400, 2, 1)

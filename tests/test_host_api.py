@@ -66,6 +66,26 @@ def test_product_never_imports_the_oracle():
             assert "oracle" not in path.read_text().lower(), path
 
 
+def test_host_index_narrowing():
+    """vbh_narrow_indices: int64 -> int32 (the halved PCIe upload of the neighbor table), -1 padding kept, values
+    that do not fit reported."""
+    from paper_2407_02740_b200.preprocess import host_library
+    lib = host_library()
+    rng = np.random.default_rng(5)
+    src = rng.integers(-1, 2 ** 31 - 1, size=100_003, dtype=np.int64)
+    src[:7] = [-1, 0, 1, 2 ** 31 - 1, 12345, -1, 7]
+    dst = np.empty(src.size, dtype=np.int32)
+    for workers in (0, 1, 3):
+        dst[:] = 99
+        assert lib.vbh_narrow_indices(src.ctypes.data, dst.ctypes.data, src.size, workers) == 0
+        assert np.array_equal(dst.astype(np.int64), src)
+    assert lib.vbh_narrow_indices(src.ctypes.data, dst.ctypes.data, 0, 0) == 0
+    big = src.copy()
+    big[50_000] = 2 ** 31
+    assert lib.vbh_narrow_indices(big.ctypes.data, dst.ctypes.data, big.size, 0) == 1
+    assert lib.vbh_narrow_indices(None, dst.ctypes.data, 4, 0) == -1
+
+
 # ---- model / covariance / preprocess ------------------------------------------
 def test_model_types_and_validation():
     ds = vg.Dataset([1, 2, 3], [1, 1, 1], [[0, 0], [1, 0], [0, 1]])
