@@ -117,8 +117,8 @@ def make_workload(n_total: int, d: int, p: int, seed: int = 2407):
     locs = rng.uniform(0.0, 1.0, (n_total, d))
     y = rng.normal(size=n_total)
     X = np.ones((n_total, p))
-    if p > 1:
-        X[:, 1:] = locs[:, :p - 1]
+    for j in range(1, p):  # covariates: the coordinates, then their squares, ... (p - 1 may exceed d)
+        X[:, j] = locs[:, (j - 1) % d] ** (1 + (j - 1) // d)
     return y, X, locs
 
 

@@ -494,6 +494,10 @@ static __device__ __noinline__ void vb_finish_impl(const FinishArgs E, const int
         E.out[o] = vb_fixed_sum(E.group_sums + o, (int)ng, (size_t)L);
     for (unsigned t = threadIdx.x; t < ng + 1; t += blockDim.x)
         E.tickets[t] = 0u;
+#ifdef TILED_DYNAMIC
+    if (threadIdx.x == 0)
+        E.tickets[VB_FINISH_MAXGROUPS] = 0u; // the batch counter of the dynamic-schedule experiment
+#endif
     if (threadIdx.x == 0) {
         const unsigned int cnt = *E.fail_count;
         const unsigned long long w = *E.fail_word;

@@ -36,7 +36,7 @@
 // -DVB200_EXPERIMENTS (tools/build_variant.py); the product build always uses the defaults below.
 #if !defined(VB200_EXPERIMENTS) && (defined(TILED_ABLATE) || defined(TILED_STAGGER_NS) || defined(TILED_CLOCKS) || \
                                     defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB) || \
-                                    defined(TILED_NO_SMEM_BLOCKS))
+                                    defined(TILED_NO_SMEM_BLOCKS) || defined(TILED_DYNAMIC))
 #error "TILED_* experiment knobs need -DVB200_EXPERIMENTS"
 #endif
 #ifndef TILED_WPB
@@ -304,27 +304,35 @@ __device__ __forceinline__ void phase_sync()
 //             Pairs that touch a padding row are not evaluated at all (the table lists live pairs first).
 // Everything after the pair phase is shared.
 // Resident blocks per SM the kernel is compiled for (__launch_bounds__): the register tier of the geometry, unless the
-// instance's shared memory admits 8 blocks or fewer anyway (two or three derivative matrices: space-time, general
-// Matern, anisotropic) -- then it may use the registers of those blocks instead of being held to the 168 of 12 blocks
-// (measured at n = 2^20: space-time d = 3 5.75 -> 5.47 ms, anisotropic d = 2 5.48 -> 5.05 ms; an instance that fits
-// 11 blocks, Matern-3/2 d = 3 p = 4, got slower when compiled for 11: the rule only applies at <= 8).
-template <int G, int S, int D, int QD, int NP>
+// instance's shared memory admits fewer blocks anyway -- then it is compiled for the next multiple of four at or below
+// what fits (four schedulers per SM: 11 resident warps run no faster than 8, and 8 may use 255 registers instead of
+// being held to the 168 of 12 blocks).  Measured at n = 2^20: space-time d = 3 5.75 -> 5.47 ms, anisotropic d = 2
+// 5.48 -> 5.05 ms (two derivative matrices: 8 blocks fit), Matern-3/2 d = 3 p = 4 7.24 -> 6.25 ms (11 blocks fit;
+// compiled for 11 it got slower, 7.46 ms).
+// The design columns cost registers too (1 + P right-hand sides per row, (1+Q)(2+P+P^2)+Q^2 accumulator terms spread
+// over the G lanes): measured at n = 2^20, Matern-3/2, d = 2 -- (16,2) tier, 12 -> 8 blocks: P = 1 4.28 -> 4.35 ms
+// (kept at 12), P = 2 5.00 -> 4.75, P = 3 5.19 -> 5.08, P = 4 6.39 -> 5.75; (4,3) tier, 16 / 12 / 8 blocks: P = 1
+// 0.515 / 0.581 / 0.644, P = 2 0.651 / 0.626 / 0.728, P = 3 0.818 / 0.792 / 0.831, P = 4 1.216 / 1.134 / 0.948;
+// (8,3) tier: 12 blocks at every P (P = 4: 2.98 vs 2.99, P = 2: 2.35 vs 2.64).
+template <int G, int S, int D, int QD, int NP, int P>
 __host__ __device__ constexpr int tiled_launch_blocks()
 {
-    constexpr int by_reg = tiled_min_blocks(G, S, NP);
-#if !defined(TILED_NO_SMEM_BLOCKS) && TILED_WPB == 1
+    constexpr int base = tiled_min_blocks(G, S, NP);
+#if !defined(TILED_NO_SMEM_BLOCKS) && !defined(TILED_MINB) && TILED_WPB == 1
+    constexpr int by_reg = (base == 16) ? (P >= 4 ? 8 : (P >= 2 ? 12 : 16))
+                                        : ((base == 12 && G == 16 && P >= 2) ? 8 : base);
     constexpr long long bytes = (long long)LikSmem<G, S, D, QD, NP>::TOTAL * 8 + 1024; // + the per-block reservation
     constexpr int by_smem = (int)(233472 / bytes) < 1 ? 1 : (int)(233472 / bytes);
-    return (by_smem <= 8 && by_smem < by_reg) ? by_smem : by_reg;
+    return by_smem >= by_reg ? by_reg : (by_smem >= 8 ? (by_smem / 4) * 4 : by_smem);
 #else
-    return by_reg;
+    return base;
 #endif
 }
 
 // NP > 1 (pair-table variant only): the first NP local rows are padding rows of every observation the instance
 // serves (m+1 <= CAP-NP); see TileGeom.
 template <int G, int S, int FAM, int D, int P, bool PT = false, int NP = 1>
-__global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, FamTraits<FAM, D>::QD, NP>() + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
+__global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, FamTraits<FAM, D>::QD, NP, P>() + TILED_WPB - 1) / TILED_WPB) vecchia_tiled_kernel(const EvalParams E)
 {
     static_assert(!PT || TILED_WPB == 1, "the pair-table variant runs one warp per block");
     static_assert(NP == 1 || PT, "static padding rows are implemented for the pair-table variant");
@@ -438,8 +446,21 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
     load_rec(nidx, nrec);
 #endif
     // every warp of a block runs the same number of rounds (barriers inside); surplus rounds are inactive
+#ifdef TILED_DYNAMIC
+    // experiment: batches handed out by a global counter instead of the static stride (NOT run-to-run reproducible:
+    // the batches a block sums change from launch to launch) -- measures what schedule imbalance costs
+    for (;;) {
+        unsigned int nb_ = 0;
+        if (lane == 0)
+            nb_ = atomicAdd(E.tickets + VB_FINISH_MAXGROUPS, 1u);
+        nb_ = __shfl_sync(FULLMASK, nb_, 0);
+        if ((int64_t)nb_ >= nbatch)
+            break;
+        const int64_t batch = (int64_t)nb_;
+#else
     for (int64_t batch0 = (int64_t)blockIdx.x * TILED_WPB; batch0 < nbatch; batch0 += stride) {
         const int64_t batch = batch0 + warp;
+#endif
         const int64_t i = E.i0 + batch * OPW + g;
         const bool active = i < E.i1;
 #if !TILED_PREFETCH || TILED_PREFETCH >= 4

@@ -146,6 +146,30 @@ def test_not_positive_definite_reports_observation_and_pivot(failure_case):
             fields_close(rescued, z["rescued_totals"], 1, 3, 1e-4)  # near-singular K (cond ~1e6): the two CPU oracles differ by 1.4e-5 here
 
 
+@pytest.mark.parametrize("m", [20, 40, 50, 60])
+def test_failure_report_on_exact_size_tiers(m):
+    """The exact-size tiers (static padding rows: packed triangles that start at local row NP-1) must report the same
+    (observation, pivot) as the CPU oracle for a duplicated location with zero nugget -- the pivot index is counted
+    in the observation's own frame, whatever padding the tier adds in front."""
+    from oracle import vecchia_oracle as vo_
+    rng = np.random.default_rng(300 + m)
+    n = 3 * m + 30
+    locs = rng.uniform(0.0, 1.0, (n, 2))
+    dup = 2 * m + 9
+    locs[dup] = locs[dup - 3]                # exact duplicate of an earlier point: singular local matrix
+    y, X = rng.normal(size=n), np.ones((n, 1))
+    theta = np.array([1.2, 0.3, 0.0])
+    nn = vg.find_ordered_neighbors(locs, m)
+    with pytest.raises(vo_.OracleNotPositiveDefinite) as want:
+        vo_.run(y, X, locs, nn.idx, "matern15_isotropic", theta)
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern15_isotropic") as prob:
+        prob.set_layout("tiled_reg")
+        with pytest.raises(vg.NotPositiveDefinite) as got:
+            prob.totals(theta)
+        assert "NP=" in prob.last_kernel_name, prob.last_kernel_name
+    assert (got.value.observation, got.value.pivot) == (want.value.observation, want.value.pivot)
+
+
 FAMILY_SHAPES = [
     ("exponential_isotropic", 2, 1, [1.5, 0.25, 0.1], 30),
     ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 30),

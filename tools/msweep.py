@@ -37,8 +37,9 @@ def time_m(m, n, family):
 
 
 def ncu_m(m, n, family):
-    # launches: 8 chunked launches of the first evaluation, then resident-table launches -> skip 9, capture 1
-    cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:vecchia_", "-s", "9", "-c", "1",
+    # launches: 16 chunked launches of the first evaluation (DeviceProblem's default for tables >= 32 MB), then
+    # resident-table launches -> skip 17, capture 1
+    cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:vecchia_", "-s", "17", "-c", "1",
            "--csv", sys.executable, str(ROOT / "tools" / "time_kernel.py"), "--m", str(m), "--n", str(n), "--family", family,
            "--reps", "1"]
     out = subprocess.run(cmd, capture_output=True, text=True)
@@ -62,7 +63,7 @@ def main():
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "r2_msweep.json"))
     ap.add_argument("--n", type=int, default=1 << 20)
     ap.add_argument("--family", default="matern15_isotropic")
-    ap.add_argument("--ms", default="10,20,30,40,60")
+    ap.add_argument("--ms", default="10,20,30,40,50,60")
     a = ap.parse_args()
     import bench
     res = {"n": a.n, "family": a.family, "what": "config 4 neighbor-count sweep; kernel_ms from CUDA events (no profiler), "
