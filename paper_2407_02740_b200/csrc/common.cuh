@@ -37,6 +37,12 @@ struct MaternOrder {
     double rp[VB_MATERN_TERMS]; // 1 / (i - mu)
     double rq[VB_MATERN_TERMS]; // 1 / (i + mu)
     double ra[VB_MATERN_CF];    // 1 / a_i of CF2, a_i = mu^2 - 1/4 - i(i-1), i = 2..
+    // order derivatives of the constants above (central order only): the smoothness derivative of the series branch
+    // is the ANALYTIC mu-derivative of Temme's series, carried along term by term (bessel_series_dnu)
+    double dgam1, dgam2, dfact; // d/dmu of Gamma_1, Gamma_2, pi mu / sin(pi mu)
+    double psi_p, psi_m;        // digamma(1 + mu), digamma(1 - mu): d log Gamma(1 +- mu) / d(+-mu)
+    double dlognc2;             // d log(2 / Gamma(nu)) / dnu = -digamma(nu)
+    double tm[VB_MATERN_TERMS]; // 2 mu / (i^2 - mu^2) = d log r1[i] / dmu
 };
 #define VB_MATERN_H 1e-5 // central-difference step of the smoothness derivative
 
@@ -255,6 +261,75 @@ static __device__ VB_BESSEL_ATTR void bessel_k_pair(double x, double d, double i
     }
 }
 
+// Series branch (x <= 2) of the central order WITH its analytic order derivative: every quantity of Temme's series is
+// differentiated with respect to mu alongside its value (11 more FP64 instructions per term, against 22 for the two
+// shifted orders of a central difference, and no difference quotient: the result carries no 1e-16 / 2h rounding
+// noise).  d/dnu = d/dmu at fixed nup.  Outputs as bessel_k_pair plus dtnu = d tnu / d nu.
+static __device__ __forceinline__ void bessel_series_dnu(double x, double d, double inv_x, const MaternOrder &M, const double E,
+                                                         const int nterms, double &tnu, double &bq, double &dtnu)
+{
+    const double mu = M.mu;
+    const double xh = 0.5 * x, d2 = xh * xh;
+    const double Ei = rcp_pos(E);        // (x/2)^mu = exp(-mu d)
+    const double e = mu * d, e2 = e * e;
+    const double ch = 0.5 * (E + Ei);    // cosh(e)
+    const double sh = 0.5 * (E - Ei);    // sinh(e)
+    // S = sinh(mu d) / mu and dS/dmu = (d cosh(e) - S) / mu; short series in e where the quotients cancel
+    double S, dS;
+    if (fabs(e) < 1e-2) {
+        S = d * fma(e2, fma(e2, 1.0 / 120.0, 1.0 / 6.0), 1.0);
+        dS = d * d * e * fma(e2, fma(e2, 1.0 / 840.0, 1.0 / 30.0), 1.0 / 3.0);
+    } else {
+        S = sh * M.inv_mu;
+        dS = fma(d, ch, -S) * M.inv_mu;
+    }
+    const double g0 = fma(M.gam1, ch, M.gam2 * S);
+    double ff = M.fact * g0;
+    double dff = fma(M.dfact, g0, M.fact * (fma(M.dgam1, ch, M.gam1 * d * sh) + fma(M.dgam2, S, M.gam2 * dS)));
+    double p = 0.5 * E * M.gp, q = 0.5 * Ei * M.gm;
+    double dp = p * (d + M.psi_p), dq = -q * (d + M.psi_m);
+    double sum = ff, dsum = dff, sum1 = p, dsum1 = dp, c = 1.0;
+#pragma unroll
+    for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
+        if (i > nterms)
+            break;
+        ff = fma((double)i, ff, p + q) * M.r1[i - 1];
+        dff = fma(fma((double)i, dff, dp + dq), M.r1[i - 1], ff * M.tm[i - 1]);
+        c *= d2 * (1.0 / i);
+        p *= M.rp[i - 1];
+        dp = fma(dp, M.rp[i - 1], p * M.rp[i - 1]);
+        q *= M.rq[i - 1];
+        dq = fma(dq, M.rq[i - 1], -(q * M.rq[i - 1]));
+        sum = fma(c, ff, sum);
+        dsum = fma(c, dff, dsum);
+        sum1 = fma(c, fma(-(double)i, ff, p), sum1);
+        dsum1 = fma(c, fma(-(double)i, dff, dp), dsum1);
+    }
+    const double kmu = sum, dkmu = dsum, tx = 2.0 * inv_x;
+    const double kmu1 = sum1 * tx, dkmu1 = dsum1 * tx;
+    const double s1 = Ei * xh; // (x/2)^(mu+1)
+    // T_mu = Ei kmu, T_(mu+1) = s1 kmu1; d Ei / d mu = -d Ei
+    if (M.nup == 0) {
+        tnu = Ei * kmu;
+        dtnu = Ei * fma(-d, kmu, dkmu);
+        bq = s1 * fma(-2.0 * mu * inv_x, kmu, kmu1);
+    } else {
+        double prev = Ei * kmu, cur = s1 * kmu1;
+        double dprev = Ei * fma(-d, kmu, dkmu), dcur = s1 * fma(-d, kmu1, dkmu1);
+        for (int i = 1; i < M.nup; ++i) {
+            const double next = fma(mu + i, cur, d2 * prev);
+            const double dnext = fma(mu + i, dcur, fma(d2, dprev, cur));
+            prev = cur;
+            dprev = dcur;
+            cur = next;
+            dcur = dnext;
+        }
+        tnu = cur;
+        dtnu = dcur;
+        bq = d2 * prev;
+    }
+}
+
 // Series length for this x (terms ~ (x/2)^(2i) / (i!)^2 against 1e-17), uniform over the lanes that are active
 // here (the callers' pair loops end raggedly, so the vote runs on the active mask).
 __device__ __forceinline__ int matern_series_terms(const double x)
@@ -266,9 +341,10 @@ __device__ __forceinline__ int matern_series_terms(const double x)
 }
 
 // General Matern pair terms at scaled distance x = r/range: correlation 2^(1-nu)/Gamma(nu) x^nu K_nu(x),
-// its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative by a
-// central difference of step VB_MATERN_H (part of the family definition here; GpGp differentiates the
-// smoothness numerically as well).
+// its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative: analytic (the order
+// derivative of Temme's series, bessel_series_dnu) for x <= 2, a central difference of step VB_MATERN_H for x > 2
+// (the continued-fraction branch; GpGp differentiates the smoothness numerically everywhere, and so do this
+// repository's CPU oracles -- the two agree to the O(h^2) ~ 1e-10 truncation of the difference quotient).
 __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, double inv_rho, double &Kv, double &Drange,
                                              double &Dnu)
 {
@@ -293,6 +369,17 @@ __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, doub
         return fma(z, fma(z, fma(z, fma(z, fma(z, 1.0 / 120.0, 1.0 / 24.0), 1.0 / 6.0), 0.5), 1.0), 1.0);
     };
     const double E0 = exp(P.mat[0].mu * d);
+#ifndef VB_MATERN_CENTRAL_DIFF
+    if (x <= 2.0) { // one evaluation: value, range derivative and the analytic smoothness derivative
+        double t0, b0, dt0;
+        bessel_series_dnu(x, d, inv_x, P.mat[0], E0, nterms, t0, b0, dt0);
+        const double sn = P.sig2 * P.mat[0].nc2;
+        Kv = sn * t0;
+        Drange = 2.0 * sn * b0 * inv_rho;
+        Dnu = sn * fma(P.mat[0].dlognc2, t0, dt0);
+        return;
+    }
+#endif
     const double dm1 = P.mat[1].mu - P.mat[0].mu, dm2 = P.mat[2].mu - P.mat[0].mu; // uniform
     const double E1 = (fabs(dm1) < 1e-3) ? E0 * small_exp(dm1 * d) : exp(P.mat[1].mu * d);
     const double E2 = (fabs(dm2) < 1e-3) ? E0 * small_exp(dm2 * d) : exp(P.mat[2].mu * d);

@@ -569,7 +569,10 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
             using TS = TileSmem<G, S, D, QD, NP>;
             // pairs in flight per lane: two for the closed forms; ONE for the general Matern, whose Bessel evaluations
             // are long enough to spill when two are interleaved (measured 38 ms against 50 ms per evaluation)
-            constexpr int NI = (FAM == FAM_MATERN) ? 1 : TS::NI;
+#ifndef TILED_MATERN_NI
+#define TILED_MATERN_NI 1
+#endif
+            constexpr int NI = (FAM == FAM_MATERN) ? TILED_MATERN_NI : TS::NI;
             const int nlp = nlive * (nlive - 1) / 2;
             unsigned nxt[NI];
 #pragma unroll

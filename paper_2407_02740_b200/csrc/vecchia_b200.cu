@@ -421,6 +421,19 @@ extern "C" int vb200_set_layout(vb200_problem *P, int layout)
 // Temme constants of one order (host, long double gamma): Gamma_1 = (1/G(1-mu) - 1/G(1+mu)) / (2 mu),
 // Gamma_2 = (1/G(1-mu) + 1/G(1+mu)) / 2; for tiny |mu| the odd part of the reciprocal-gamma Taylor
 // series is used: Gamma_1 -> -(euler_gamma + a3 mu^2), a3 = -0.0420026350340952.
+// digamma in long double: recurrence up to x >= 12, then the asymptotic series (error < 1e-18 there)
+static long double digammal(long double x)
+{
+    long double r = 0.0L;
+    while (x < 12.0L) {
+        r -= 1.0L / x;
+        x += 1.0L;
+    }
+    const long double f = 1.0L / (x * x);
+    return r + logl(x) - 0.5L / x -
+           f * (1.0L / 12 - f * (1.0L / 120 - f * (1.0L / 252 - f * (1.0L / 240 - f * (1.0L / 132 - f * (691.0L / 32760 - f / 12))))));
+}
+
 static MaternOrder matern_order(double nu)
 {
     MaternOrder M;
@@ -444,7 +457,32 @@ static MaternOrder matern_order(double nu)
     M.normcon = std::exp((1.0 - nu) * 0.6931471805599453 - std::lgamma(nu));
     M.nc2 = std::exp(0.6931471805599453 - std::lgamma(nu));
     M.inv_mu = M.mu != 0.0 ? 1.0 / M.mu : 0.0;
+    // order derivatives (bessel_series_dnu): d(1/G(1+mu)) = -psi(1+mu)/G(1+mu), d(1/G(1-mu)) = +psi(1-mu)/G(1-mu)
+    {
+        const long double psp = digammal(1.0L + mu), psm = digammal(1.0L - mu);
+        M.psi_p = (double)psp;
+        M.psi_m = (double)psm;
+        M.dgam2 = (double)(0.5L * (psm * gm - psp * gp));
+        if (fabsl(mu) < 1e-2L) {
+            // Gamma_1 = -(a2 + a4 mu^2 + a6 mu^4 + a8 mu^6 + ...), a_k the coefficients of 1/Gamma(z) = sum a_k z^k
+            const long double a4 = -0.0420026350340952355L, a6 = -0.0421977345555443367L, a8 = 0.0072189432466630995L;
+            const long double m2 = mu * mu;
+            M.dgam1 = (double)(-mu * (2.0L * a4 + m2 * (4.0L * a6 + m2 * 6.0L * a8)));
+        } else {
+            const long double g1 = (gm - gp) / (2.0L * mu);
+            M.dgam1 = (double)(((psm * gm + psp * gp) - 2.0L * g1) / (2.0L * mu));
+        }
+        if (fabsl(pimu) < 1e-2L) { // pi mu / sin(pi mu) = 1 + t^2/6 + 7 t^4/360 + 31 t^6/15120, t = pi mu
+            const long double pi = 3.14159265358979323846264338L, t2 = pimu * pimu;
+            M.dfact = (double)(pi * pimu * (1.0L / 3 + t2 * (7.0L / 90 + t2 * 31.0L / 2520)));
+        } else {
+            const long double pi = 3.14159265358979323846264338L;
+            M.dfact = (double)((pimu / sinl(pimu)) * (1.0L / mu - pi * cosl(pimu) / sinl(pimu)));
+        }
+        M.dlognc2 = (double)(-digammal((long double)nu));
+    }
     for (int i = 1; i <= VB_MATERN_TERMS; ++i) {
+        M.tm[i - 1] = (double)(2.0L * mu / ((long double)i * i - mu * mu));
         M.r1[i - 1] = (double)(1.0L / ((long double)i * i - mu * mu));
         M.rp[i - 1] = (double)(1.0L / ((long double)i - mu));
         M.rq[i - 1] = (double)(1.0L / ((long double)i + mu));
