@@ -344,7 +344,7 @@ __device__ __forceinline__ int matern_series_terms(const double x)
 // its range derivative sigma^2 nc x^(nu+1) K_{nu-1}(x) / range, and the smoothness derivative: analytic (the order
 // derivative of Temme's series, bessel_series_dnu) for x <= 2, a central difference of step VB_MATERN_H for x > 2
 // (the continued-fraction branch; GpGp differentiates the smoothness numerically everywhere, and so do this
-// repository's CPU oracles -- the two agree to the O(h^2) ~ 1e-10 truncation of the difference quotient).
+// repository's CPU restatements used by the tests -- the two agree to the O(h^2) ~ 1e-10 truncation of the difference quotient).
 __device__ __forceinline__ void matern_terms(const EvalParams &P, double x, double inv_rho, double &Kv, double &Drange,
                                              double &Dnu)
 {
