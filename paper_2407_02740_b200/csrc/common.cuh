@@ -67,6 +67,7 @@ struct EvalParams {
     int ws_doubles;          // per-warp scratch doubles (warp_smem layout)
     const unsigned int *pair_tab; // tiled layout: off-diagonal pair table of the tier (device memory)
     int sm_count;            // SMs of the device (tiled layout: start stagger of the resident blocks)
+    int prefetch;            // tiled layout: 1 = the point records exceed L2, request the next batch's inputs ahead
     unsigned long long *dbg_clocks; // experiments only (-DTILED_CLOCKS): per-phase cycle sums; nullptr otherwise
     // in-kernel finish (vb_finish below): the evaluation is ONE launch
     double *out;             // result vector, L+2 doubles (totals, failure count, -(first failing index)-1)

@@ -466,9 +466,14 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
 #if !TILED_PREFETCH || TILED_PREFETCH >= 4
         load_idx(batch, nidx);
         load_rec(nidx, nrec);
-#if TILED_PREFETCH >= 4
-        // register-free: the index row of this warp's NEXT batch is requested into L2 (4) / L1 (6) now
-        {
+#if TILED_PREFETCH >= 4 || TILED_PREFETCH == 0
+        // register-free: the index row of this warp's NEXT batch is requested into L2 (4) / L1 (6) now.  Product
+        // build (TILED_PREFETCH == 0): behind the run-time flag E.prefetch, which the host sets when the point
+        // records do not fit L2 (then the gather is an HBM round trip per neighbor instead of an L2 hit: measured at
+        // n = 2^22, d = 3, p = 4: 27.2 -> 24.8 ms; at n = 2^20, where the records are L2-resident, it costs 1-2 %)
+        // (not compiled into the d = 2, p = 1 instances: their 32-byte records fit L2 up to n = 2^21, and the extra
+        // block costs the headline kernel 2 % through register allocation alone)
+        if (TILED_PREFETCH >= 4 || (RV > 4 && E.prefetch)) {
             const int64_t inx = i + stride * OPW;
             if (inx < E.i1) {
                 const int64_t *nrow = E.nn + (inx - E.nn_row0) * E.mp1;
@@ -1078,10 +1083,11 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
         for (int s = 0; s < S; ++s)
             if (nidx[s] >= 0)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(E.rec + nidx[s] * E.rs));
-#elif TILED_PREFETCH == 5
+#elif TILED_PREFETCH == 5 || TILED_PREFETCH == 0
         // the next batch's indices come from L2 by now (requested at the top of this batch); its records are
-        // requested into L1 and the indices dropped again (nothing is held across the batch boundary)
-        {
+        // requested into L1 and the indices dropped again (nothing is held across the batch boundary).  Product
+        // build: instances with design columns only (their records span two sectors), behind E.prefetch
+        if (TILED_PREFETCH == 5 || (P > 1 && E.prefetch)) {
             int64_t pidx[S];
             load_idx(batch + stride, pidx);
 #pragma unroll

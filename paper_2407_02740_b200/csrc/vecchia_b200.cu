@@ -749,7 +749,8 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
                               [&](size_t rows) -> double * {
                                   return ensure_partials(P, partial_doubles(rows, 1, E.L)) == VB200_OK ? P->partials
                                                                                                        : nullptr;
-                              });
+                              },
+                              (size_t)P->n * (size_t)P->rs * sizeof(double));
             if (rc == -100)
                 return fail(VB200_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(cudaGetLastError()));
             if (rc)
