@@ -337,8 +337,16 @@ __device__ __forceinline__ int matern_series_terms(const double x)
 {
     const unsigned am = __activemask();
     const bool valid = x <= 2.0;
+#ifdef VB_MATERN_FULL_SERIES
     return __any_sync(am, valid && x > 1.0) ? VB_MATERN_TERMS
            : (__any_sync(am, valid && x > 0.4) ? 10 : (__any_sync(am, valid && x > 0.1) ? 7 : 5));
+#else
+    // first neglected term, (x/2)^(2i) / (i!)^2 at i = nterms + 1, below 1e-14 of the leading one (the covariance
+    // needs ~1e-12): 10 / 7 / 5 / 4 terms (6e-16, 9e-15, 8e-15, 7e-18 at the upper end of each bracket); round 2a
+    // ran 12 / 10 / 7 / 5 (1e-19 ... 1e-24)
+    return __any_sync(am, valid && x > 1.0) ? 10
+           : (__any_sync(am, valid && x > 0.4) ? 7 : (__any_sync(am, valid && x > 0.1) ? 5 : 4));
+#endif
 }
 
 // General Matern pair terms at scaled distance x = r/range: correlation 2^(1-nu)/Gamma(nu) x^nu K_nu(x),

@@ -36,7 +36,7 @@
 // -DVB200_EXPERIMENTS (tools/build_variant.py); the product build always uses the defaults below.
 #if !defined(VB200_EXPERIMENTS) && (defined(TILED_ABLATE) || defined(TILED_STAGGER_NS) || defined(TILED_CLOCKS) || \
                                     defined(TILED_HEAD_SHFL) || defined(TILED_WPB) || defined(TILED_MINB) || \
-                                    defined(TILED_NO_SMEM_BLOCKS) || defined(TILED_DYNAMIC))
+                                    defined(TILED_NO_SMEM_BLOCKS) || defined(TILED_DYNAMIC) || defined(TILED_RHS_LATE))
 #error "TILED_* experiment knobs need -DVB200_EXPERIMENTS"
 #endif
 #ifndef TILED_WPB
@@ -64,6 +64,10 @@
 #endif
 #ifndef TILED_BD
 #define TILED_BD 4 // column-store loads in flight ahead of the back-substitution chain
+#endif
+#ifndef TILED_RHS_LATE
+#define TILED_RHS_LATE 0 // 1: the forward substitutions of y and X run in the sweep loop after the back-substitution
+                         // (next to [D_r u, u]) instead of inside the factorization sweep
 #endif
 #ifndef TILED_RNI
 #define TILED_RNI 4 // independent pair evaluations in flight per lane (row-owner pair phase)
@@ -573,7 +577,9 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
             //      k(k-1)/2 pairs among the live points come first; the rest is zero-filled. ----
             using TS = TileSmem<G, S, D, QD, NP>;
             // pairs in flight per lane: two for the closed forms; ONE for the general Matern, whose Bessel evaluations
-            // are long enough to spill when two are interleaved (measured 38 ms against 50 ms per evaluation)
+            // are long enough to spill when two are interleaved (measured 38 ms against 50 ms per evaluation with the
+            // three-order central difference; with the analytic smoothness derivative 20.1 against 27.0 ms, and with
+            // the NI series sharing one term loop 18.5 / 22.1 / 33.5 / 31.7 ms for NI = 1 / 2 / 3 / 4)
 #ifndef TILED_MATERN_NI
 #define TILED_MATERN_NI 1
 #endif
@@ -738,7 +744,8 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
                     KLs[Geo::colbase(j) + rowi[s]] = Kr[s][j];
 #pragma unroll
             for (int r = 0; r < 1 + P; ++r)
-                xr[r] = __shfl_sync(FULLMASK, rhs[r][sj], oj, G);
+                if (!TILED_RHS_LATE)
+                    xr[r] = __shfl_sync(FULLMASK, rhs[r][sj], oj, G);
             __syncwarp();
             const double *col = KLs + Geo::colbase(j);
             const int cs = ((Geo::colbase(j) + j) & 1) ? j + 1 : j;
@@ -817,7 +824,7 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
                 for (int r = 0; r < 1 + P; ++r)
 #pragma unroll
                     for (int s = 0; s < S; ++s)
-                        if ((s + 1) * G - 1 > j)
+                        if (!TILED_RHS_LATE && (s + 1) * G - 1 > j)
                             rhs[r][s] = fma(-Lc[s], xr[r], rhs[r][s]);
 #pragma unroll
                 for (int s = 0; s < S; ++s)
@@ -1052,6 +1059,16 @@ __global__ void __launch_bounds__(32 * TILED_WPB, (tiled_launch_blocks<G, S, D, 
                     if ((s + 1) * G - 1 > j)
                         rr[r][s] = fma(-Lm[s], x, rr[r][s]);
             }
+#if TILED_RHS_LATE
+#pragma unroll
+            for (int r = 0; r < 1 + P; ++r) {
+                const double x = __shfl_sync(FULLMASK, rhs[r][sj], oj, G);
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if ((s + 1) * G - 1 > j)
+                        rhs[r][s] = fma(-Lm[s], x, rhs[r][s]);
+            }
+#endif
         }
         // Now, with <a,b> = sum_a a_a b_a / d_a and s = 1/sqrt(d_e):
         //   z = D^-1/2 yt, W = D^-1/2 Xt            (yt = rhs[0], Xt = rhs[1+b])
