@@ -57,6 +57,24 @@ __global__ void pack_records_kernel(const double *y, const double *X, const doub
         r[t] = 0.0;
 }
 
+// Design-column padding (enqueue_eval): a shape whose p has no register-tiled instance runs the instance of the next
+// larger p on records whose extra design columns are zero -- every accumulator entry that involves a padded column
+// is then exactly zero and the others are untouched -- and the result vector is gathered back to the layout of p.
+__global__ void repack_records_kernel(const double *rec, int rs, int keep, double *out, int rs_out, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    for (int t = 0; t < rs_out; ++t)
+        out[i * rs_out + t] = (t < keep) ? rec[i * rs + t] : 0.0;
+}
+
+__global__ void gather_result_kernel(const double *src, const int *map, double *dst, int count)
+{
+    for (int o = threadIdx.x; o < count; o += blockDim.x)
+        dst[o] = src[map[o]];
+}
+
 // The partial rows are added inside the main kernel (vb_finish, common.cuh): one launch per evaluation.
 // An evaluation over an empty range still has to produce its result vector:
 __global__ void empty_result_kernel(double *out, int L)
@@ -156,6 +174,14 @@ struct vb200_problem {
     size_t smem_optin = 0;
     bool timing = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // design-column padding (see repack_records_kernel): records with pad_p >= p design columns, the result vector of
+    // the padded evaluation and the gather map back to p (built per (pad_p, q))
+    double *rec_pad = nullptr;
+    int pad_p = 0, rs_pad = 0;
+    double *out_pad = nullptr;
+    size_t out_pad_cap = 0;
+    int *map_dev = nullptr;
+    int map_q = 0, map_len = 0;
 };
 
 static bool is_device_ptr(const void *ptr)
@@ -386,6 +412,9 @@ extern "C" int vb200_destroy(vb200_problem *P)
     if (P->d_out) cudaFreeAsync(P->d_out, P->stream);
     if (P->fail_word) cudaFreeAsync(P->fail_word, P->stream);
     if (P->tickets) cudaFreeAsync(P->tickets, P->stream);
+    if (P->rec_pad) cudaFreeAsync(P->rec_pad, P->stream);
+    if (P->out_pad) cudaFreeAsync(P->out_pad, P->stream);
+    if (P->map_dev) cudaFreeAsync(P->map_dev, P->stream);
     if (P->h_out) cudaFreeHost(P->h_out);
     if (P->h_fail) cudaFreeHost(P->h_fail);
     if (P->ev0) cudaEventDestroy(P->ev0);
@@ -706,12 +735,89 @@ static int launch_thread(vb200_problem *P, EvalParams &E, bool smem_tri, int *nb
     return VB200_OK;
 }
 
+// The p the register-tiled layout runs this problem with: its own, or the next larger one that has an instance
+// (design columns padded with zeros); 0 if none.
+static int tiled_effective_p(const vb200_problem *P, int family)
+{
+    for (int pe = P->p; pe <= 4; ++pe)
+        if (tiled_find(family, P->mp1, pe, P->d) != nullptr)
+            return pe;
+    return 0;
+}
+
 static int resolve_layout(const vb200_problem *P, int family, int q)
 {
     int layout = P->layout;
+    (void)q;
     if (layout == VB200_LAYOUT_AUTO)
-        layout = tiled_supported(family, P->mp1, P->p, P->d, q) ? VB200_LAYOUT_TILED_REG : VB200_LAYOUT_WARP_SMEM;
+        layout = tiled_effective_p(P, family) ? VB200_LAYOUT_TILED_REG : VB200_LAYOUT_WARP_SMEM;
     return layout;
+}
+
+// Records with pe design columns (zeros beyond p), the padded result vector and the gather map for (pe, q).
+static int ensure_padding(vb200_problem *P, int pe, int q)
+{
+    if (P->pad_p != pe) {
+        if (P->rec_pad) {
+            CUDA_TRY(cudaFreeAsync(P->rec_pad, P->stream));
+            P->rec_pad = nullptr;
+        }
+        P->rs_pad = (P->d + 1 + pe + 1) & ~1;
+        CUDA_TRY(vb_malloc_async(&P->rec_pad, sizeof(double) * (size_t)P->n * P->rs_pad, P->stream));
+        const int bs = 256;
+        const unsigned grid = (unsigned)((P->n + bs - 1) / bs);
+        repack_records_kernel<<<grid, bs, 0, P->stream>>>(P->rec, P->rs, P->d + 1 + P->p, P->rec_pad, P->rs_pad, P->n);
+        CUDA_TRY(cudaGetLastError());
+        P->pad_p = pe;
+        P->map_q = 0;
+    }
+    const int Lp = vb200_acc_len(pe, q), L = vb200_acc_len(P->p, q);
+    if (P->out_pad_cap < (size_t)Lp + 2) {
+        if (P->out_pad)
+            CUDA_TRY(cudaFreeAsync(P->out_pad, P->stream));
+        CUDA_TRY(vb_malloc_async(&P->out_pad, sizeof(double) * ((size_t)Lp + 2), P->stream));
+        P->out_pad_cap = (size_t)Lp + 2;
+    }
+    if (P->map_q != q) {
+        const int p = P->p;
+        const AccLayout A(p, q), B(pe, q);
+        std::vector<int> map((size_t)L + 2);
+        map[0] = 0;
+        map[1] = 1;
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b)
+                map[A.xsx + a * p + b] = B.xsx + a * pe + b;
+        for (int b = 0; b < p; ++b)
+            map[A.ysx + b] = B.ysx + b;
+        for (int j = 0; j < q; ++j) {
+            map[A.dlogdet + j] = B.dlogdet + j;
+            map[A.dysy + j] = B.dysy + j;
+        }
+        for (int b = 0; b < p; ++b)
+            for (int j = 0; j < q; ++j)
+                map[A.dysx + b * q + j] = B.dysx + b * q + j;
+        for (int a = 0; a < p; ++a)
+            for (int b = 0; b < p; ++b)
+                for (int j = 0; j < q; ++j)
+                    map[A.dxsx + (a * p + b) * q + j] = B.dxsx + (a * pe + b) * q + j;
+        for (int j = 0; j < q * q; ++j)
+            map[A.ainfo + j] = B.ainfo + j;
+        map[L] = Lp;          // failure count
+        map[L + 1] = Lp + 1;  // -(first failing index) - 1
+        if (P->map_dev && P->map_len < L + 2) {
+            CUDA_TRY(cudaFreeAsync(P->map_dev, P->stream));
+            P->map_dev = nullptr;
+        }
+        if (!P->map_dev) {
+            CUDA_TRY(vb_malloc_async(&P->map_dev, sizeof(int) * ((size_t)L + 2), P->stream));
+            P->map_len = L + 2;
+        }
+        // pageable source: the copy has returned from the host buffer when the call returns
+        CUDA_TRY(cudaMemcpyAsync(P->map_dev, map.data(), sizeof(int) * ((size_t)L + 2), cudaMemcpyHostToDevice, P->stream));
+        CUDA_TRY(cudaStreamSynchronize(P->stream));
+        P->map_q = q;
+    }
+    return VB200_OK;
 }
 
 extern "C" int vb200_get_layout(const vb200_problem *P, int family, int q)
@@ -737,24 +843,45 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
     P->last_launches = 0;
     int nblocks = 0;
     if (i1 > i0) {
-        const int layout = resolve_layout(P, family, q);
+        int layout = resolve_layout(P, family, q);
+        // per-observation rows (diagnostics) are laid out for p: a padded-p evaluation cannot write them
+        if (P->layout == VB200_LAYOUT_AUTO && layout == VB200_LAYOUT_TILED_REG && (d_rows || d_fail_rows) &&
+            tiled_effective_p(P, family) != P->p)
+            layout = VB200_LAYOUT_WARP_SMEM;
         if (P->layout == VB200_LAYOUT_AUTO && layout == VB200_LAYOUT_WARP_SMEM)
             ++g_fallback_evals;
         if (P->timing)
             CUDA_TRY(cudaEventRecord(P->ev0, P->stream));
         if (layout == VB200_LAYOUT_TILED_REG) {
-            if (!tiled_supported(family, P->mp1, P->p, P->d, q))
+            const int pe = tiled_effective_p(P, family);
+            if (!pe)
                 return fail(VB200_EUNSUPPORTED, "TILED_REG layout does not support this shape");
+            if (pe != P->p) { // no instance for this p: the next larger one on zero-padded design columns
+                if (d_rows || d_fail_rows)
+                    return fail(VB200_EUNSUPPORTED, "per-observation rows need a TILED_REG instance for this p");
+                if ((rc = ensure_padding(P, pe, q)))
+                    return rc;
+                E.rec = P->rec_pad;
+                E.rs = P->rs_pad;
+                E.p = pe;
+                E.L = vb200_acc_len(pe, q);
+                E.out = P->out_pad;
+            }
             rc = launch_tiled(P->stream, P->sm_count, P->smem_optin, E, &nblocks, &P->last_kernel,
                               [&](size_t rows) -> double * {
                                   return ensure_partials(P, partial_doubles(rows, 1, E.L)) == VB200_OK ? P->partials
                                                                                                        : nullptr;
                               },
-                              (size_t)P->n * (size_t)P->rs * sizeof(double));
+                              (size_t)P->n * (size_t)E.rs * sizeof(double));
             if (rc == -100)
                 return fail(VB200_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(cudaGetLastError()));
             if (rc)
                 return fail(rc, "tiled launch failed");
+            if (pe != P->p) {
+                gather_result_kernel<<<1, 128, 0, P->stream>>>(P->out_pad, P->map_dev, d_out, vb200_acc_len(P->p, q) + 2);
+                CUDA_TRY(cudaGetLastError());
+                P->last_launches++;
+            }
         } else if (layout == VB200_LAYOUT_WARP_SMEM) {
             rc = launch_warp_smem(P, E, &nblocks);
             if (rc)

@@ -170,6 +170,38 @@ def test_failure_report_on_exact_size_tiers(m):
     assert (got.value.observation, got.value.pivot) == (want.value.observation, want.value.pivot)
 
 
+@pytest.mark.parametrize("p", [2, 3])
+def test_design_column_padding_serves_p_without_an_instance(p):
+    """m = 40 has register-tiled instances for p = 1 and p = 4 only: p = 2, 3 must run the p = 4 instance on
+    zero-padded design columns (not the generic kernel) and reproduce the oracle's totals field by field; the
+    per-observation rows (laid out for p) still come from the generic kernel."""
+    from paper_2407_02740_b200 import _cabi
+    y, X, locs, _ = make_instance(500 + p, 700, 2, p)
+    theta = np.array([1.1, 0.2, 0.07])
+    nn = vg.find_ordered_neighbors(locs, 40)
+    want = vo.run(y, X, locs, nn.idx, "matern15_isotropic", theta)
+    before = _cabi.load().vb200_fallback_count()
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, "matern15_isotropic") as prob:
+        assert prob.layout_for(3) == "tiled_reg"
+        got = prob.totals(theta)
+        assert "P=4" in prob.last_kernel_name and "NP=7" in prob.last_kernel_name, prob.last_kernel_name
+        again = prob.totals(theta, i0=100, i1=650) + prob.totals(theta, i0=0, i1=100) + prob.totals(theta, i0=650, i1=700)
+        assert _cabi.load().vb200_fallback_count() == before
+        rows, flags = prob.rows_host(theta)
+    fields_close(got, want, p, 3, 1e-9)
+    fields_close(again, want, p, 3, 1e-9)
+    fields_close(rows.sum(axis=0), want, p, 3, 1e-9)
+    assert not flags.any()
+    # failure propagation through the gathered result vector
+    locs2 = locs.copy()
+    locs2[650] = locs2[640]
+    nn2 = vg.find_ordered_neighbors(locs2, 40)
+    with DeviceProblem(vg.Dataset(y, X, locs2), nn2, "matern15_isotropic") as prob:
+        with pytest.raises(vg.NotPositiveDefinite) as err:
+            prob.totals(np.array([1.1, 0.2, 0.0]))
+        assert err.value.observation == 650
+
+
 FAMILY_SHAPES = [
     ("exponential_isotropic", 2, 1, [1.5, 0.25, 0.1], 30),
     ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 30),
