@@ -60,13 +60,25 @@ __global__ void pack_records_kernel(const double *y, const double *X, const doub
 // Design-column padding (enqueue_eval): a shape whose p has no register-tiled instance runs the instance of the next
 // larger p on records whose extra design columns are zero -- every accumulator entry that involves a padded column
 // is then exactly zero and the others are untouched -- and the result vector is gathered back to the layout of p.
-__global__ void repack_records_kernel(const double *rec, int rs, int keep, double *out, int rs_out, int64_t n)
+// Likewise an isotropic family in fewer coordinates than any instance has (d = 1) runs a d = 2 instance on records with
+// a zero coordinate appended: the distances are unchanged.
+// out record = { locs[0..d), 0 x (d_out - d), y, X[0..p), 0 ... }
+__global__ void repack_records_kernel(const double *rec, int rs, int d, int p, double *out, int rs_out, int d_out,
+                                      int64_t n)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
-    for (int t = 0; t < rs_out; ++t)
-        out[i * rs_out + t] = (t < keep) ? rec[i * rs + t] : 0.0;
+    const double *r = rec + i * rs;
+    double *o = out + i * rs_out;
+    for (int t = 0; t < rs_out; ++t) {
+        double v = 0.0;
+        if (t < d)
+            v = r[t];
+        else if (t >= d_out && t - d_out <= p) // y and the p design columns
+            v = r[d + (t - d_out)];
+        o[t] = v;
+    }
 }
 
 __global__ void gather_result_kernel(const double *src, const int *map, double *dst, int count)
@@ -177,7 +189,7 @@ struct vb200_problem {
     // design-column padding (see repack_records_kernel): records with pad_p >= p design columns, the result vector of
     // the padded evaluation and the gather map back to p (built per (pad_p, q))
     double *rec_pad = nullptr;
-    int pad_p = 0, rs_pad = 0;
+    int pad_p = 0, pad_d = 0, rs_pad = 0;
     double *out_pad = nullptr;
     size_t out_pad_cap = 0;
     int *map_dev = nullptr;
@@ -735,14 +747,26 @@ static int launch_thread(vb200_problem *P, EvalParams &E, bool smem_tri, int *nb
     return VB200_OK;
 }
 
-// The p the register-tiled layout runs this problem with: its own, or the next larger one that has an instance
-// (design columns padded with zeros); 0 if none.
+// The (d, p) the register-tiled layout runs this problem with: its own, or -- design columns padded with zeros, and for
+// the isotropic families coordinates padded with zeros -- the nearest larger shape that has an instance; false if none.
+static bool tiled_effective_shape(const vb200_problem *P, int family, int *de_out, int *pe_out)
+{
+    const bool iso = family == VB200_EXP_ISO || family == VB200_MATERN15 || family == VB200_MATERN25 ||
+                     family == VB200_MATERN;
+    for (int de = P->d; de <= (iso ? 3 : P->d); ++de)
+        for (int pe = P->p; pe <= 4; ++pe)
+            if (tiled_find(family, P->mp1, pe, de) != nullptr) {
+                if (de_out) *de_out = de;
+                if (pe_out) *pe_out = pe;
+                return true;
+            }
+    return false;
+}
+
 static int tiled_effective_p(const vb200_problem *P, int family)
 {
-    for (int pe = P->p; pe <= 4; ++pe)
-        if (tiled_find(family, P->mp1, pe, P->d) != nullptr)
-            return pe;
-    return 0;
+    int de = 0, pe = 0;
+    return tiled_effective_shape(P, family, &de, &pe) ? pe : 0;
 }
 
 static int resolve_layout(const vb200_problem *P, int family, int q)
@@ -754,21 +778,23 @@ static int resolve_layout(const vb200_problem *P, int family, int q)
     return layout;
 }
 
-// Records with pe design columns (zeros beyond p), the padded result vector and the gather map for (pe, q).
-static int ensure_padding(vb200_problem *P, int pe, int q)
+// Records with de coordinates and pe design columns (zeros beyond d and p), the padded result vector and the gather
+// map for (pe, q).
+static int ensure_padding(vb200_problem *P, int de, int pe, int q)
 {
-    if (P->pad_p != pe) {
+    if (P->pad_p != pe || P->pad_d != de) {
         if (P->rec_pad) {
             CUDA_TRY(cudaFreeAsync(P->rec_pad, P->stream));
             P->rec_pad = nullptr;
         }
-        P->rs_pad = (P->d + 1 + pe + 1) & ~1;
+        P->rs_pad = (de + 1 + pe + 1) & ~1;
         CUDA_TRY(vb_malloc_async(&P->rec_pad, sizeof(double) * (size_t)P->n * P->rs_pad, P->stream));
         const int bs = 256;
         const unsigned grid = (unsigned)((P->n + bs - 1) / bs);
-        repack_records_kernel<<<grid, bs, 0, P->stream>>>(P->rec, P->rs, P->d + 1 + P->p, P->rec_pad, P->rs_pad, P->n);
+        repack_records_kernel<<<grid, bs, 0, P->stream>>>(P->rec, P->rs, P->d, P->p, P->rec_pad, P->rs_pad, de, P->n);
         CUDA_TRY(cudaGetLastError());
         P->pad_p = pe;
+        P->pad_d = de;
         P->map_q = 0;
     }
     const int Lp = vb200_acc_len(pe, q), L = vb200_acc_len(P->p, q);
@@ -853,19 +879,25 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
         if (P->timing)
             CUDA_TRY(cudaEventRecord(P->ev0, P->stream));
         if (layout == VB200_LAYOUT_TILED_REG) {
-            const int pe = tiled_effective_p(P, family);
-            if (!pe)
+            int de = 0, pe = 0;
+            if (!tiled_effective_shape(P, family, &de, &pe))
                 return fail(VB200_EUNSUPPORTED, "TILED_REG layout does not support this shape");
-            if (pe != P->p) { // no instance for this p: the next larger one on zero-padded design columns
-                if (d_rows || d_fail_rows)
+            const bool padded = pe != P->p || de != P->d;
+            if (padded) { // no instance for this (d, p): the nearest larger one on zero-padded records
+                if ((d_rows || d_fail_rows) && pe != P->p)
                     return fail(VB200_EUNSUPPORTED, "per-observation rows need a TILED_REG instance for this p");
-                if ((rc = ensure_padding(P, pe, q)))
+                if ((rc = ensure_padding(P, de, pe, q)))
                     return rc;
                 E.rec = P->rec_pad;
                 E.rs = P->rs_pad;
-                E.p = pe;
-                E.L = vb200_acc_len(pe, q);
-                E.out = P->out_pad;
+                for (int l = P->d; l < de; ++l)
+                    E.inv_rho[l] = E.inv_rho[0]; // isotropic families only (tiled_effective_shape)
+                E.d = de;
+                if (pe != P->p) {
+                    E.p = pe;
+                    E.L = vb200_acc_len(pe, q);
+                    E.out = P->out_pad;
+                }
             }
             rc = launch_tiled(P->stream, P->sm_count, P->smem_optin, E, &nblocks, &P->last_kernel,
                               [&](size_t rows) -> double * {
@@ -877,7 +909,7 @@ static int enqueue_eval(vb200_problem *P, int family, const double *theta, int q
                 return fail(VB200_ECUDA, std::string("tiled launch: ") + cudaGetErrorString(cudaGetLastError()));
             if (rc)
                 return fail(rc, "tiled launch failed");
-            if (pe != P->p) {
+            if (padded && pe != P->p) {
                 gather_result_kernel<<<1, 128, 0, P->stream>>>(P->out_pad, P->map_dev, d_out, vb200_acc_len(P->p, q) + 2);
                 CUDA_TRY(cudaGetLastError());
                 P->last_launches++;

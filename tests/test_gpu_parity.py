@@ -202,6 +202,35 @@ def test_design_column_padding_serves_p_without_an_instance(p):
         assert err.value.observation == 650
 
 
+@pytest.mark.parametrize("family,theta", [("exponential_isotropic", [1.2, 0.05, 0.1]),
+                                          ("matern15_isotropic", [1.2, 0.03, 0.1]),
+                                          ("matern_isotropic", [1.2, 0.04, 0.9, 0.1])])
+def test_one_dimensional_locations_run_the_two_dimensional_instances(family, theta):
+    """d = 1 (a time series): no instance is compiled for one coordinate; the isotropic families run the d = 2
+    instance on records with a zero coordinate appended (same distances) instead of the generic kernel."""
+    from paper_2407_02740_b200 import _cabi
+    rng = np.random.default_rng(91)
+    n, p = 900, 2
+    locs = np.sort(rng.uniform(0.0, 1.0, (n, 1)), axis=0)[rng.permutation(n)]
+    X = np.column_stack([np.ones(n), rng.normal(size=n)])
+    y = rng.normal(size=n) + np.sin(5.0 * locs[:, 0])
+    theta = np.asarray(theta)
+    nn = vg.find_ordered_neighbors(locs, 30)
+    want = vo.run(y, X, locs, nn.idx, family, theta)
+    before = _cabi.load().vb200_fallback_count()
+    with DeviceProblem(vg.Dataset(y, X, locs), nn, family) as prob:
+        got = prob.totals(theta)
+        assert "D=2" in prob.last_kernel_name and "vecchia_tiled_kernel" in prob.last_kernel_name
+        assert _cabi.load().vb200_fallback_count() == before
+        # (the general Matern has instances for p = 1, 4 only: its p = 2 rows come from the generic kernel)
+        rows, flags = prob.rows_host(theta)
+    q = theta.shape[0]
+    tol = 1e-8 if family == "matern_isotropic" else 1e-9
+    fields_close(got, want, p, q, tol)
+    fields_close(rows.sum(axis=0), want, p, q, tol)
+    assert not flags.any()
+
+
 FAMILY_SHAPES = [
     ("exponential_isotropic", 2, 1, [1.5, 0.25, 0.1], 30),
     ("matern15_isotropic", 2, 1, [1.0, 0.08, 0.1], 30),
