@@ -20,6 +20,11 @@
 //     for u = B^-T e_last, into which the symmetric mat-vec D_r u is fused.
 // The forward substitutions of y and X ride along inside the factorization sweep.
 //
+// Exact-size instances (template parameter NP, pair-table variant): an instance may declare its first NP local rows
+// padding rows of EVERY observation it serves (m+1 <= CAP-NP); the shared-memory triangles are then packed for
+// CAP-NP+1 rows and the column loops start at NP -- fewer bytes per observation, more resident warps (TileGeom).
+// How many resident blocks an instance is compiled for: tiled_launch_blocks below (measured rules).
+//
 // Rows with fewer than CAP live points (local row 0 always; the ragged head rows i < m; m+1 < CAP-1)
 // are padding rows at the FRONT of the local frame: unit diagonal, zero data, and coordinates 1e30
 // scaled units away from everything (distinct per row), so every pair term that touches them
