@@ -134,7 +134,10 @@ __host__ __device__ constexpr int tiled_min_blocks(int G, int S, int NP = 1)
 #ifdef TILED_MINB
     return TILED_MINB; // development knob
 #else
-    return (G * S * (S + 1) <= 48) ? 16 : ((G * S * (S + 1) <= 96) ? 12 : 8);
+    // 32-bit registers of the row entries a lane keeps: slot s holds columns NP-1 .. (s+1)G-1 of its row
+    int regs = 0;
+    for (int s = 0; s < S; ++s)
+        regs += 2 * (((s + 1) * G - (NP - 1)) > 0 ? ((s + 1) * G - (NP - 1)) : 0);
+    return (regs <= 56) ? 16 : ((regs <= 96) ? 12 : 8);
 #endif
 }
-

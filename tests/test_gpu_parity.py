@@ -146,7 +146,7 @@ def test_not_positive_definite_reports_observation_and_pivot(failure_case):
             fields_close(rescued, z["rescued_totals"], 1, 3, 1e-4)  # near-singular K (cond ~1e6): the two CPU oracles differ by 1.4e-5 here
 
 
-@pytest.mark.parametrize("m", [20, 40, 50, 60])
+@pytest.mark.parametrize("m", [15, 20, 25, 40, 50, 60])
 def test_failure_report_on_exact_size_tiers(m):
     """The exact-size tiers (static padding rows: packed triangles that start at local row NP-1) must report the same
     (observation, pivot) as the CPU oracle for a duplicated location with zero nugget -- the pivot index is counted

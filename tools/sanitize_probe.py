@@ -13,6 +13,7 @@ for family, d, p, theta, m in [("matern15_isotropic", 2, 1, [1.0, 0.1, 0.1], 30)
                                # exact-size tiers (static padding rows): m = 20 / 50 / 60, and a ragged m on each
                                ("matern15_isotropic", 2, 1, [1.0, 0.1, 0.1], 20), ("matern15_isotropic", 2, 1, [1.0, 0.1, 0.1], 50),
                                ("matern15_isotropic", 2, 1, [1.0, 0.1, 0.1], 60), ("exponential_isotropic", 2, 4, [1.0, 0.1, 0.1], 37),
+                               ("matern25_isotropic", 2, 1, [1.0, 0.1, 0.1], 15), ("exponential_spacetime", 3, 4, [1, .2, .5, .1], 25),
                                ("matern_isotropic", 3, 1, [1.0, 0.3, 2.2, 0.1], 40)]:
     n = 600
     locs = rng.uniform(0, 1, (n, d)); y = rng.normal(size=n)
