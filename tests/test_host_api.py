@@ -66,6 +66,25 @@ def test_product_never_imports_the_oracle():
             assert "oracle" not in path.read_text().lower(), path
 
 
+def test_every_baseline_shape_has_a_register_tiled_instance():
+    """The instance registry (readable without a GPU) must cover the shapes BASELINE.json names -- exact-size
+    instances for the neighbor-count sweep of config 4 -- so that none of them drops to the generic kernel."""
+    inst = _cabi.tiled_instances()  # (lanes, rows_per_lane, cap, family_code, d, p); serves m+1 <= cap-1
+    fam = {"exponential_isotropic": 0, "exponential_spacetime": 2, "matern15_isotropic": 3, "matern_isotropic": 5}
+
+    def best_cap(family, d, p, m):
+        caps = [c for (_, _, c, f, dd, pp) in inst if f == fam[family] and dd == d and pp == p and c - 1 >= m + 1]
+        return min(caps) if caps else None
+
+    assert best_cap("exponential_isotropic", 2, 1, 30) == 32                      # config 1
+    for m, cap in ((10, 12), (15, 17), (20, 22), (25, 27), (30, 32), (40, 42), (50, 52), (60, 62)):
+        assert best_cap("matern15_isotropic", 2, 1, m) == cap, m                  # configs 2 and 4 (+ m = 15, 25, 50)
+    assert best_cap("matern_isotropic", 2, 1, 30) == 32                           # config 2 as literally named
+    assert best_cap("exponential_spacetime", 3, 1, 30) == 32                      # config 3
+    assert best_cap("matern15_isotropic", 3, 4, 30) == 32                         # config 5
+    assert best_cap("matern15_isotropic", 2, 1, 62) == 64 and best_cap("matern15_isotropic", 2, 1, 63) is None
+
+
 def test_host_index_narrowing():
     """vbh_narrow_indices: int64 -> int32 (the halved PCIe upload of the neighbor table), -1 padding kept, values
     that do not fit reported."""
